@@ -1,0 +1,344 @@
+"""B200-native evaluation path of arXiv 2004.08177's data-driven DVFS scheduler.
+
+Python host mirror of the reference's predictor/scheduler interface for the
+hot path, calling the sm_100a kernels through the C ABI (include/gdvfs.h):
+
+=====================================  ==========================================
+reference (proj/)                      here
+=====================================  ==========================================
+models::predict (models.cpp:395)       :func:`predict` / :meth:`Model.predict`
+models::load_model_file (:710)         :meth:`Model.load_file`
+make_model_predictor + build           :func:`grid_select` (rows generated on
+  (scheduler.cpp:329-394)                the fly, E/T fused with selection)
+select_text / select_literal /         :func:`select` (K3 over given E/T),
+  best effort (scheduler.cpp:62-100)     fused in :func:`grid_select`
+schedule_d_dvfs + run_edf_loop         :func:`schedule_d_dvfs`
+  (scheduler.cpp:105-147, 182-237)
+=====================================  ==========================================
+
+Errors map to the reference's exception types: ``ValueError`` for
+std::invalid_argument, :class:`DataError` for data_error,
+:class:`MissingArtifactError` for missing_artifact_error.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import GdError
+from .workload import Forest, GridInputs
+
+__all__ = [
+    "Context", "Model", "SchedulerOptions", "DECISION_DTYPE", "predict", "grid_select", "select",
+    "schedule_d_dvfs", "DataError", "MissingArtifactError", "GdError", "Forest", "GridInputs",
+]
+
+MODE = {"text": 0, "text_semantics": 0, "literal": 1, "literal_pseudocode": 1}
+OBJECTIVE = {"energy": 0, "power": 1}
+BUDGET = {"remaining": 0, "remaining_time": 0, "full": 1, "full_deadline": 1}
+
+DECISION_DTYPE = np.dtype([("clock_index", "<i4"), ("status", "<i4"), ("note", "<i4"), ("pad", "<i4"),
+                           ("energy_ws", "<f8"), ("time_s", "<f8")])
+JOB_DTYPE = np.dtype([("arrival_s", "<f8"), ("deadline_s", "<f8"), ("app_rank", "<i8"), ("app_index", "<i4"),
+                      ("pad", "<i4")])
+
+
+class DataError(RuntimeError):
+    """gpudvfs::data_error (core.hpp:20-23)."""
+
+
+class MissingArtifactError(RuntimeError):
+    """gpudvfs::missing_artifact_error (core.hpp:26-29)."""
+
+
+def _raise(rc: int) -> None:
+    if rc == _capi.GD_OK:
+        return
+    msg = _capi.lib().gd_last_error().decode()
+    if rc == _capi.GD_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == _capi.GD_ERR_DATA:
+        raise DataError(msg)
+    if rc == _capi.GD_ERR_MISSING_ARTIFACT:
+        raise MissingArtifactError(msg)
+    raise GdError(rc, msg)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def _c(a, dtype) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+@dataclasses.dataclass
+class SchedulerOptions:
+    """SchedulerOptions (scheduler.hpp:62-67); defaults match the reference."""
+
+    mode: str = "text"
+    budget: str = "remaining"
+    objective: str = "energy"
+    best_effort_fallback: bool = False
+
+    def opts(self) -> _capi.SelectOpts:
+        return _capi.SelectOpts(MODE[self.mode], OBJECTIVE[self.objective], int(self.best_effort_fallback), 0)
+
+
+class Context:
+    """One CUDA device + stream (gd_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_ctx_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        _raise(_capi.lib().gd_ctx_set_stream(self._h, stream_ptr))
+
+    def synchronize(self) -> None:
+        _raise(_capi.lib().gd_ctx_synchronize(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(_capi.lib().gd_ctx_launch_count(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            _capi.lib().gd_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class Model:
+    """A device-resident, packed ensemble (or linear model)."""
+
+    def __init__(self, handle, ctx: Context):
+        self._h = handle
+        self.ctx = ctx
+        info = _capi.ModelInfo()
+        _raise(_capi.lib().gd_model_info_get(handle, C.byref(info)))
+        self.kind, self.target, self.n_cols = info.kind, info.target, info.n_cols
+        self.n_trees, self.n_nodes, self.max_depth = info.n_trees, info.n_nodes, info.max_depth
+        self.base, self.learning_rate = info.base_prediction, info.learning_rate
+
+    @classmethod
+    def from_forest(cls, forest: Forest, ctx: Optional[Context] = None, host_only: bool = False) -> "Model":
+        """Pack + upload an ensemble (host_only: pack and validate without a device)."""
+        ctx = None if host_only else (ctx or default_context())
+        keep = [_c(forest.tree_offsets, np.int64), _c(forest.feature, np.int32), _c(forest.threshold, np.float64),
+                _c(forest.left, np.int32), _c(forest.right, np.int32), _c(forest.leaf_value, np.float64)]
+        view = _capi.ForestView(forest.n_trees, *[k.ctypes.data for k in keep])
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_model_upload_gbt(ctx.handle if ctx else None, C.byref(view), float(forest.base),
+                                               float(forest.learning_rate), int(forest.n_cols), int(forest.target),
+                                               C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def linear(cls, coef, intercept: float, kind: str = "ols", target: int = 0,
+               ctx: Optional[Context] = None) -> "Model":
+        ctx = ctx or default_context()
+        coef = _c(coef, np.float64)
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_model_upload_linear(ctx.handle, _ptr(coef), coef.shape[0], float(intercept),
+                                                  {"ols": 0, "lasso": 1}[kind], target, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def load_file(cls, path: str, ctx: Optional[Context] = None, host_only: bool = False) -> "Model":
+        """load_model_file (models.cpp:710-714) straight into the packer."""
+        ctx = None if host_only else (ctx or default_context())
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_model_load_file(ctx.handle if ctx else None, str(path).encode(), C.byref(h)))
+        return cls(h, ctx)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def columns(self) -> Sequence[str]:
+        out = []
+        for j in range(self.n_cols):
+            s = _capi.lib().gd_model_column(self._h, j)
+            if s is None:
+                return []
+            out.append(s.decode())
+        return out
+
+    def export(self) -> Forest:
+        off = np.empty(self.n_trees + 1, np.int64)
+        n = self.n_nodes
+        f, l, r = (np.empty(n, np.int32) for _ in range(3))
+        th, lv = np.empty(n, np.float64), np.empty(n, np.float64)
+        _raise(_capi.lib().gd_model_export(self._h, _ptr(off), _ptr(f), _ptr(th), _ptr(l), _ptr(r), _ptr(lv)))
+        return Forest(off, f, th, l, r, lv, self.base, self.learning_rate, self.target, self.n_cols)
+
+    def predict(self, rows, leaf_ids: bool = False):
+        return predict(self, rows, leaf_ids=leaf_ids)
+
+    def close(self) -> None:
+        if self._h:
+            _capi.lib().gd_model_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def predict(model: Model, rows, leaf_ids: bool = False, columns: Optional[Sequence[str]] = None):
+    """models::predict (models.cpp:395-428) on the GPU (kernel K1).
+
+    ``columns`` (optional) reproduces the reference's column-name check and
+    its std::invalid_argument message (models.cpp:396-412) for models that
+    carry names (loaded from a model file).
+    """
+    if columns is not None and model.columns:
+        _check_columns(list(model.columns), list(columns))
+    rows = _c(rows, np.float64)
+    if rows.ndim != 2:
+        raise ValueError("predict: rows must be a 2-D array")
+    out = np.empty(rows.shape[0], np.float64)
+    ids = np.empty((rows.shape[0], model.n_trees), np.int32) if leaf_ids else None
+    _raise(_capi.lib().gd_predict_rows(model.ctx.handle, model.handle, _ptr(rows), rows.shape[0], rows.shape[1],
+                                       _ptr(out), _ptr(ids)))
+    return (out, ids) if leaf_ids else out
+
+
+def _check_columns(model_cols, row_cols):
+    if len(model_cols) != len(row_cols):
+        limit = min(len(model_cols), len(row_cols))
+        for j in range(limit):
+            if model_cols[j] != row_cols[j]:
+                raise ValueError(f"predict: column mismatch at '{row_cols[j]}' (model expects '{model_cols[j]}')")
+        longer = model_cols if len(model_cols) > len(row_cols) else row_cols
+        raise ValueError(f"predict: column mismatch at '{longer[limit]}'")
+    for m, r in zip(model_cols, row_cols):
+        if m != r:
+            raise ValueError(f"predict: column mismatch at '{r}' (model expects '{m}')")
+
+
+def _grid_struct(grid: GridInputs, budgets: np.ndarray, keep: list) -> _capi.Grid:
+    rows = _c(grid.rows, np.float64)
+    cat_t = _c(grid.cat_t, np.float64)
+    cat_cols = _c(grid.cat_cols, np.int32)
+    rec = None if grid.rec_of_clock is None else _c(grid.rec_of_clock, np.int32)
+    sm, mem = _c(grid.sm, np.int32), _c(grid.mem, np.int32)
+    keep += [rows, cat_t, cat_cols, rec, sm, mem, budgets]
+    return _capi.Grid(_ptr(rows), rows.shape[0], rows.shape[1], cat_cols.shape[0], _ptr(cat_t), _ptr(cat_cols),
+                      _ptr(rec), grid.n_apps, _ptr(sm), _ptr(mem), sm.shape[0], grid.sm_col, grid.mem_col, 0,
+                      _ptr(budgets))
+
+
+def grid_select(energy: Model, time: Model, grid: GridInputs, budgets, options: Optional[SchedulerOptions] = None,
+                return_predictions: bool = False, out: Optional[np.ndarray] = None):
+    """Fused K2+K3: E and T for every (app, clock) candidate, then the
+    per-app deadline-masked selection.  Returns a DECISION_DTYPE array (and
+    the A x C E/T tables when ``return_predictions``).  Host arrays may be
+    pinned (e.g. torch pin_memory views); ``out`` reuses a result buffer."""
+    options = options or SchedulerOptions(budget="full")
+    budgets = _c(budgets, np.float64)
+    keep: list = []
+    g = _grid_struct(grid, budgets, keep)
+    a, c = grid.n_apps, grid.n_clocks
+    if out is None:
+        out = np.zeros(a, DECISION_DTYPE)
+    elif out.dtype != DECISION_DTYPE or out.shape != (a,) or not out.flags.c_contiguous:
+        raise ValueError("grid_select: out must be a contiguous DECISION_DTYPE array of n_apps")
+    e = np.empty((a, c), np.float64) if return_predictions else None
+    t = np.empty((a, c), np.float64) if return_predictions else None
+    opts = options.opts()
+    _raise(_capi.lib().gd_grid_select(energy.ctx.handle, energy.handle, time.handle, C.byref(g), C.byref(opts),
+                                      _ptr(out), _ptr(e), _ptr(t)))
+    return (out, e, t) if return_predictions else out
+
+
+def select(energy_table, time_table, sm, budgets, options: Optional[SchedulerOptions] = None,
+           ctx: Optional[Context] = None):
+    """K3 alone over given candidate tables (e.g. the truth predictor)."""
+    ctx = ctx or default_context()
+    options = options or SchedulerOptions(budget="full")
+    e, t = _c(energy_table, np.float64), _c(time_table, np.float64)
+    sm, budgets = _c(sm, np.int32), _c(budgets, np.float64)
+    out = np.zeros(e.shape[0], DECISION_DTYPE)
+    opts = options.opts()
+    _raise(_capi.lib().gd_select(ctx.handle, _ptr(e), _ptr(t), e.shape[0], _ptr(sm), sm.shape[0], _ptr(budgets),
+                                 C.byref(opts), _ptr(out)))
+    return out
+
+
+def make_jobs(arrival, deadline, app_rank, app_index) -> np.ndarray:
+    jobs = np.zeros(len(arrival), JOB_DTYPE)
+    jobs["arrival_s"], jobs["deadline_s"] = arrival, deadline
+    jobs["app_rank"], jobs["app_index"] = app_rank, app_index
+    return jobs
+
+
+def schedule_d_dvfs(jobs: np.ndarray, energy_table, time_table, sm, exec_time,
+                    options: Optional[SchedulerOptions] = None):
+    """schedule_d_dvfs over per-app E/T tables (from :func:`grid_select`):
+    EDF order, remaining/full budgets, selection per job.  Returns
+    (decisions in processing order, job index of each decision)."""
+    options = options or SchedulerOptions()
+    jobs = np.ascontiguousarray(jobs, JOB_DTYPE)
+    e, t = _c(energy_table, np.float64), _c(time_table, np.float64)
+    sm = _c(sm, np.int32)
+    ex = _c(exec_time, np.float64)
+    n = jobs.shape[0]
+    out = np.zeros(n, DECISION_DTYPE)
+    order = np.zeros(n, np.int64)
+    opts = options.opts()
+    _raise(_capi.lib().gd_schedule_edf(_ptr(jobs), n, _ptr(e), _ptr(t), _ptr(sm), sm.shape[0], BUDGET[options.budget],
+                                       C.byref(opts), _ptr(ex), _capi.EXEC_FN(), None, _ptr(out), _ptr(order)))
+    return out, order
+
+
+def grid_select_device(energy: Model, time: Model, d: dict, n_apps: int, n_clocks: int, n_cols: int, n_cat: int,
+                       sm_col: int, mem_col: int, options: Optional[SchedulerOptions] = None, e_out: int = 0,
+                       t_out: int = 0, n_records: Optional[int] = None) -> None:
+    """Enqueue the fused kernel on device-resident inputs (raw device pointers
+    in ``d``: rows, cat_t, cat_cols, rec_of_clock, sm, mem, budgets, out).
+    Returns immediately; work runs on the context's stream."""
+    options = options or SchedulerOptions(budget="full")
+    g = _capi.Grid(d["rows"], n_apps if n_records is None else n_records, n_cols, n_cat, d.get("cat_t"),
+                   d.get("cat_cols"), d.get("rec_of_clock"), n_apps, d["sm"], d["mem"], n_clocks, sm_col, mem_col, 0,
+                   d["budgets"])
+    opts = options.opts()
+    _raise(_capi.lib().gd_grid_select_device(energy.ctx.handle, energy.handle, time.handle, C.byref(g),
+                                             C.byref(opts), d["out"], e_out or None, t_out or None))
+
+
+def microbench_dadd(ctx: Optional[Context] = None) -> float:
+    """Measured FP64 add throughput of the device (adds/s)."""
+    ctx = ctx or default_context()
+    v = C.c_double()
+    _raise(_capi.lib().gd_microbench_dadd(ctx.handle, C.byref(v)))
+    return float(v.value)

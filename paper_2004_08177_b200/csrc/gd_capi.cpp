@@ -1,0 +1,624 @@
+// gd_capi.cpp -- the thin C ABI over the sm_100a kernels (include/gdvfs.h).
+//
+// Host-buffer entry points stage inputs with stream-ordered allocations
+// (cudaMallocAsync from a pool that keeps its memory), enqueue the kernel
+// and copy results back before returning.  *_device entry points take
+// device pointers and only enqueue.  There is no CPU compute fallback: a
+// missing/failed device is an error (GD_ERR_CUDA).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gd_device.cuh"
+#include "gd_host.hpp"
+
+namespace gdh {
+
+thread_local std::string g_error;
+
+int set_error(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+int cuda_error(cudaError_t e, const char* where) {
+    return set_error(GD_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace gdh
+
+using gdh::cuda_error;
+using gdh::set_error;
+
+#define GD_CUDA(call, where)                                   \
+    do {                                                       \
+        cudaError_t _e = (call);                               \
+        if (_e != cudaSuccess) return cuda_error(_e, where);   \
+    } while (0)
+
+namespace {
+
+// One stream-ordered scratch allocation carved into aligned pieces.
+struct Scratch {
+    cudaStream_t stream;
+    char* base = nullptr;
+    size_t size = 0;
+    std::vector<std::pair<size_t, size_t>> pieces;  // offset, bytes
+
+    size_t add(size_t bytes) {
+        size = (size + 255) & ~static_cast<size_t>(255);
+        pieces.push_back({size, bytes});
+        size += bytes;
+        return pieces.size() - 1;
+    }
+    void* ptr(size_t i) const { return pieces[i].second ? base + pieces[i].first : nullptr; }
+    cudaError_t alloc() { return size ? cudaMallocAsync(reinterpret_cast<void**>(&base), size, stream) : cudaSuccess; }
+    ~Scratch() {
+        if (base) cudaFreeAsync(base, stream);
+    }
+};
+
+int activate(gd_ctx* ctx) {
+    if (!ctx) return set_error(GD_ERR_INVALID_ARGUMENT, "null gd_ctx");
+    GD_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    return GD_OK;
+}
+
+int check_model(const gd_model* m, const char* who) {
+    if (!m) return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": null model");
+    if (!m->ctx) return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": host-only model (no gd_ctx)");
+    return GD_OK;
+}
+
+// Model creation accepts ctx == NULL: the model is parsed / packed /
+// validated on the host only (used by CPU-side tooling and tests).
+int activate_opt(gd_ctx* ctx) { return ctx ? activate(ctx) : GD_OK; }
+
+int upload_model(gd_model* m) {
+    if (m->kind == GD_KIND_GBT) {
+        gd_forest_view v{m->n_trees(), m->offsets.data(), m->feature.data(), m->threshold.data(),
+                         m->left.data(),  m->right.data(),   m->leaf.data()};
+        std::vector<gd::PNode> nodes;
+        std::vector<int32_t> roots;
+        int rc = gdh::pack_forest(v, m->n_cols, nodes, roots, m->max_depth);
+        if (rc) return rc;
+        m->packed_nodes = static_cast<int64_t>(nodes.size());
+        if (!m->ctx) return GD_OK;  // host-only model: validated, never uploaded
+        if (!nodes.empty()) {
+            GD_CUDA(cudaMalloc(&m->d_nodes, nodes.size() * sizeof(gd::PNode)), "cudaMalloc(nodes)");
+            GD_CUDA(cudaMemcpy(m->d_nodes, nodes.data(), nodes.size() * sizeof(gd::PNode), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(nodes)");
+        }
+        if (!roots.empty()) {
+            GD_CUDA(cudaMalloc(&m->d_roots, roots.size() * sizeof(int32_t)), "cudaMalloc(roots)");
+            GD_CUDA(cudaMemcpy(m->d_roots, roots.data(), roots.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(roots)");
+        }
+    } else {
+        if (m->ctx && !m->coef.empty()) {
+            GD_CUDA(cudaMalloc(&m->d_coef, m->coef.size() * sizeof(double)), "cudaMalloc(coef)");
+            GD_CUDA(cudaMemcpy(m->d_coef, m->coef.data(), m->coef.size() * sizeof(double), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(coef)");
+        }
+    }
+    return GD_OK;
+}
+
+void release_model(gd_model* m) {
+    if (m->d_nodes) cudaFree(m->d_nodes);
+    if (m->d_roots) cudaFree(m->d_roots);
+    if (m->d_coef) cudaFree(m->d_coef);
+    m->d_nodes = nullptr;
+    m->d_roots = nullptr;
+    m->d_coef = nullptr;
+}
+
+int predict_rows_impl(gd_ctx* ctx, const gd_model* m, const double* d_rows, int64_t n_rows, int32_t n_cols,
+                      double* d_out, int32_t* d_leaf) {
+    if (n_cols != m->n_cols) {
+        char buf[128];
+        std::snprintf(buf, sizeof(buf), "predict: column mismatch (model expects %d columns, rows have %d)", m->n_cols,
+                      n_cols);
+        return set_error(GD_ERR_INVALID_ARGUMENT, buf);
+    }
+    if (n_rows == 0) return GD_OK;
+    const int clamp = m->target == GD_TARGET_ENERGY ? 1 : 0;
+    int e;
+    if (m->kind == GD_KIND_GBT) {
+        if (n_cols > gd::kMaxCols) return set_error(GD_ERR_UNSUPPORTED, "predict: more than 1024 columns");
+        e = gd::launch_predict_gbt(m->d_nodes, m->d_roots, m->n_trees(), m->base, m->lr, clamp, d_rows, n_rows, n_cols,
+                                   d_out, d_leaf, ctx->sm_count, ctx->stream);
+    } else {
+        e = gd::launch_predict_linear(m->d_coef, m->base, clamp, d_rows, n_rows, n_cols, d_out, ctx->sm_count,
+                                      ctx->stream);
+    }
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "predict kernel launch");
+    return GD_OK;
+}
+
+int validate_grid(const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o) {
+    if (!g || !o) return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null grid/options");
+    if (me->kind != GD_KIND_GBT || mt->kind != GD_KIND_GBT) {
+        return set_error(GD_ERR_UNSUPPORTED, "grid_select: energy and time models must be GBT ensembles");
+    }
+    if (me->target != GD_TARGET_ENERGY || mt->target != GD_TARGET_TIME) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: expected an energy model and a time model");
+    }
+    if (g->n_cols != me->n_cols || g->n_cols != mt->n_cols) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "predict: column mismatch between grid rows and models");
+    }
+    if (g->n_cols <= 0 || g->n_cols > gd::kMaxCols) return set_error(GD_ERR_UNSUPPORTED, "grid_select: bad column count");
+    if (g->n_clocks <= 0 || g->n_clocks > gd::kMaxClocks) {
+        return set_error(GD_ERR_UNSUPPORTED, "grid_select: clock catalog must hold 1..512 clocks");
+    }
+    if (g->n_apps < 0 || g->n_records < 0 || g->n_cat < 0 || g->n_cat > g->n_cols) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: negative sizes");
+    }
+    if (!g->rec_of_clock && g->n_records < g->n_apps) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: one record per app required without rec_of_clock");
+    }
+    if (g->sm_col >= g->n_cols || g->mem_col >= g->n_cols || g->sm_col < -1 || g->mem_col < -1) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: clock column out of range");
+    }
+    if (o->mode != GD_MODE_TEXT && o->mode != GD_MODE_LITERAL) return set_error(GD_ERR_INVALID_ARGUMENT, "bad mode");
+    if (o->objective != GD_OBJECTIVE_ENERGY && o->objective != GD_OBJECTIVE_POWER) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "bad objective");
+    }
+    return GD_OK;
+}
+
+int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
+              gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t) {
+    gd::GridParams p{};
+    p.e_nodes = me->d_nodes;
+    p.e_roots = me->d_roots;
+    p.e_trees = me->n_trees();
+    p.e_base = me->base;
+    p.e_lr = me->lr;
+    p.t_nodes = mt->d_nodes;
+    p.t_roots = mt->d_roots;
+    p.t_trees = mt->n_trees();
+    p.t_base = mt->base;
+    p.t_lr = mt->lr;
+    p.rows = g.rows;
+    p.rows_t = d_rows_t;
+    p.cat_t = g.cat_t;
+    p.cat_cols = g.cat_cols;
+    p.rec_of_clock = g.rec_of_clock;
+    p.sm = g.sm_clock;
+    p.mem = g.mem_clock;
+    p.budgets = g.budgets;
+    p.out = d_out;
+    p.e_out = d_e;
+    p.t_out = d_t;
+    p.n_apps = g.n_apps;
+    p.n_cols = g.n_cols;
+    p.n_cat = g.n_cat;
+    p.n_clocks = g.n_clocks;
+    p.sm_col = g.sm_col;
+    p.mem_col = g.mem_col;
+    p.mode = o.mode;
+    p.objective = o.objective;
+    p.best_effort = o.best_effort;
+    if (g.n_apps == 0) return GD_OK;
+    const bool general = g.rec_of_clock != nullptr;
+    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");
+    return GD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gd_last_error(void) { return gdh::g_error.c_str(); }
+
+const char* gd_version(void) { return "gdvfs-b200 0.1 (sm_100a)"; }
+
+int gd_ctx_create(int32_t device, gd_ctx** out) {
+    if (!out) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_ctx_create: null out");
+    *out = nullptr;
+    int n = 0;
+    GD_CUDA(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_ctx_create: no such device");
+    GD_CUDA(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    GD_CUDA(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) {
+        return set_error(GD_ERR_CUDA, std::string("gd_ctx_create: sm_100a kernels need a Blackwell GPU, found ") +
+                                          prop.name);
+    }
+    auto* c = new gd_ctx;
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_error(e, "cudaStreamCreate");
+    }
+    c->stream = c->own;
+    // Keep stream-ordered scratch in the pool between calls.
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    *out = c;
+    return GD_OK;
+}
+
+int gd_ctx_destroy(gd_ctx* ctx) {
+    if (!ctx) return GD_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->own) {
+        cudaStreamSynchronize(ctx->own);
+        cudaStreamDestroy(ctx->own);
+    }
+    delete ctx;
+    return GD_OK;
+}
+
+int gd_ctx_set_stream(gd_ctx* ctx, void* stream) {
+    if (!ctx) return set_error(GD_ERR_INVALID_ARGUMENT, "null gd_ctx");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    return GD_OK;
+}
+
+int gd_ctx_synchronize(gd_ctx* ctx) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+    return GD_OK;
+}
+
+int64_t gd_ctx_launch_count(const gd_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int gd_model_upload_gbt(gd_ctx* ctx, const gd_forest_view* f, double base, double lr, int32_t n_cols, int32_t target,
+                        gd_model** out) {
+    if (!out || !f) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_upload_gbt: null argument");
+    *out = nullptr;
+    int rc = activate_opt(ctx);
+    if (rc) return rc;
+    if (n_cols < 0) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_upload_gbt: negative column count");
+    if (target != GD_TARGET_ENERGY && target != GD_TARGET_TIME) return set_error(GD_ERR_INVALID_ARGUMENT, "bad target");
+    if (f->n_trees < 0 || (f->n_trees > 0 && !f->tree_offsets)) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_upload_gbt: bad tree offsets");
+    }
+    auto* m = new gd_model;
+    m->ctx = ctx;
+    m->kind = GD_KIND_GBT;
+    m->target = target;
+    m->n_cols = n_cols;
+    m->base = base;
+    m->lr = lr;
+    const int64_t n_nodes = f->n_trees > 0 ? f->tree_offsets[f->n_trees] - f->tree_offsets[0] : 0;
+    m->offsets.assign(f->tree_offsets, f->tree_offsets + f->n_trees + 1);
+    if (f->n_trees == 0) m->offsets.assign(1, 0);
+    const int64_t o0 = m->offsets.front();
+    for (auto& o : m->offsets) o -= o0;
+    if (n_nodes > 0) {
+        m->feature.assign(f->feature + o0, f->feature + o0 + n_nodes);
+        m->threshold.assign(f->threshold + o0, f->threshold + o0 + n_nodes);
+        m->left.assign(f->left + o0, f->left + o0 + n_nodes);
+        m->right.assign(f->right + o0, f->right + o0 + n_nodes);
+        m->leaf.assign(f->leaf_value + o0, f->leaf_value + o0 + n_nodes);
+    }
+    rc = upload_model(m);
+    if (rc) {
+        release_model(m);
+        delete m;
+        return rc;
+    }
+    *out = m;
+    return GD_OK;
+}
+
+int gd_model_upload_linear(gd_ctx* ctx, const double* coef, int32_t n_cols, double intercept, int32_t kind,
+                           int32_t target, gd_model** out) {
+    if (!out || (n_cols > 0 && !coef) || n_cols < 0) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_upload_linear: bad argument");
+    }
+    *out = nullptr;
+    int rc = activate_opt(ctx);
+    if (rc) return rc;
+    if (kind != GD_KIND_OLS && kind != GD_KIND_LASSO) return set_error(GD_ERR_INVALID_ARGUMENT, "bad linear kind");
+    auto* m = new gd_model;
+    m->ctx = ctx;
+    m->kind = kind;
+    m->target = target;
+    m->n_cols = n_cols;
+    m->base = intercept;
+    m->coef.assign(coef, coef + n_cols);
+    m->offsets.assign(1, 0);
+    rc = upload_model(m);
+    if (rc) {
+        release_model(m);
+        delete m;
+        return rc;
+    }
+    *out = m;
+    return GD_OK;
+}
+
+int gd_model_load_file(gd_ctx* ctx, const char* path, gd_model** out) {
+    if (!out) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_load_file: null out");
+    *out = nullptr;
+    int rc = activate_opt(ctx);
+    if (rc) return rc;
+    auto* m = new gd_model;
+    m->ctx = ctx;
+    rc = gdh::parse_model_file(path, *m);
+    if (!rc) rc = upload_model(m);
+    if (rc) {
+        release_model(m);
+        delete m;
+        return rc;
+    }
+    *out = m;
+    return GD_OK;
+}
+
+int gd_model_info_get(const gd_model* m, gd_model_info* out) {
+    if (!m || !out) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_info_get: null argument");
+    out->kind = m->kind;
+    out->target = m->target;
+    out->n_cols = m->n_cols;
+    out->n_trees = m->n_trees();
+    out->n_nodes = static_cast<int64_t>(m->feature.size());
+    out->max_depth = m->max_depth;
+    out->pad = 0;
+    out->base_prediction = m->base;
+    out->learning_rate = m->lr;
+    return GD_OK;
+}
+
+const char* gd_model_column(const gd_model* m, int32_t j) {
+    if (!m || j < 0 || static_cast<size_t>(j) >= m->columns.size()) return nullptr;
+    return m->columns[static_cast<size_t>(j)].c_str();
+}
+
+int gd_model_export(const gd_model* m, int64_t* tree_offsets, int32_t* feature, double* threshold, int32_t* left,
+                    int32_t* right, double* leaf_value) {
+    if (!m) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_export: null model");
+    if (tree_offsets) std::memcpy(tree_offsets, m->offsets.data(), m->offsets.size() * sizeof(int64_t));
+    if (feature) std::memcpy(feature, m->feature.data(), m->feature.size() * sizeof(int32_t));
+    if (threshold) std::memcpy(threshold, m->threshold.data(), m->threshold.size() * sizeof(double));
+    if (left) std::memcpy(left, m->left.data(), m->left.size() * sizeof(int32_t));
+    if (right) std::memcpy(right, m->right.data(), m->right.size() * sizeof(int32_t));
+    if (leaf_value) std::memcpy(leaf_value, m->leaf.data(), m->leaf.size() * sizeof(double));
+    return GD_OK;
+}
+
+int gd_model_free(gd_model* m) {
+    if (!m) return GD_OK;
+    if (m->ctx) cudaSetDevice(m->ctx->device);
+    release_model(m);
+    delete m;
+    return GD_OK;
+}
+
+int gd_predict_rows_device(gd_ctx* ctx, const gd_model* m, const double* d_rows, int64_t n_rows, int32_t n_cols,
+                           double* d_out, int32_t* d_leaf) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if ((rc = check_model(m, "predict"))) return rc;
+    if (n_rows < 0 || (n_rows > 0 && (!d_rows || !d_out))) return set_error(GD_ERR_INVALID_ARGUMENT, "predict: bad rows");
+    return predict_rows_impl(ctx, m, d_rows, n_rows, n_cols, d_out, d_leaf);
+}
+
+int gd_predict_rows(gd_ctx* ctx, const gd_model* m, const double* rows, int64_t n_rows, int32_t n_cols, double* out,
+                    int32_t* leaf_ids) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if ((rc = check_model(m, "predict"))) return rc;
+    if (n_rows < 0 || (n_rows > 0 && (!rows || !out))) return set_error(GD_ERR_INVALID_ARGUMENT, "predict: bad rows");
+    if (n_cols != m->n_cols) return predict_rows_impl(ctx, m, nullptr, 0, n_cols, nullptr, nullptr);
+    if (n_rows == 0) return GD_OK;
+    Scratch s{ctx->stream};
+    const size_t i_rows = s.add(static_cast<size_t>(n_rows) * n_cols * sizeof(double));
+    const size_t i_out = s.add(static_cast<size_t>(n_rows) * sizeof(double));
+    const size_t i_leaf = s.add(leaf_ids ? static_cast<size_t>(n_rows) * m->n_trees() * sizeof(int32_t) : 0);
+    GD_CUDA(s.alloc(), "cudaMallocAsync");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_rows), rows, static_cast<size_t>(n_rows) * n_cols * sizeof(double),
+                            cudaMemcpyHostToDevice, ctx->stream),
+            "H2D rows");
+    rc = predict_rows_impl(ctx, m, static_cast<double*>(s.ptr(i_rows)), n_rows, n_cols,
+                           static_cast<double*>(s.ptr(i_out)), static_cast<int32_t*>(s.ptr(i_leaf)));
+    if (rc) return rc;
+    GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_out), static_cast<size_t>(n_rows) * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream),
+            "D2H out");
+    if (leaf_ids && m->n_trees() > 0) {
+        GD_CUDA(cudaMemcpyAsync(leaf_ids, s.ptr(i_leaf), static_cast<size_t>(n_rows) * m->n_trees() * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, ctx->stream),
+                "D2H leaf ids");
+    }
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "predict sync");
+    return GD_OK;
+}
+
+int gd_grid_select_device(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g,
+                          const gd_select_opts* o, gd_decision* d_out, double* d_e, double* d_t) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if ((rc = check_model(me, "grid_select")) || (rc = check_model(mt, "grid_select"))) return rc;
+    if ((rc = validate_grid(me, mt, g, o))) return rc;
+    if (!d_out) return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null decisions");
+    const double* rows_t = nullptr;
+    Scratch s{ctx->stream};
+    if (g->rec_of_clock && g->n_records > 0) {
+        const size_t i_rt = s.add(static_cast<size_t>(g->n_records) * g->n_cols * sizeof(double));
+        GD_CUDA(s.alloc(), "cudaMallocAsync");
+        rows_t = static_cast<double*>(s.ptr(i_rt));
+        int e = gd::launch_build_rows_t(g->rows, g->cat_t, g->cat_cols, g->n_cat, g->n_records, g->n_cols,
+                                        const_cast<double*>(rows_t), ctx->stream);
+        ++ctx->launches;
+        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
+    }
+    return grid_impl(ctx, me, mt, *g, *o, d_out, d_e, d_t, rows_t);
+}
+
+int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
+                   gd_decision* out, double* e_out, double* t_out) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if ((rc = check_model(me, "grid_select")) || (rc = check_model(mt, "grid_select"))) return rc;
+    if ((rc = validate_grid(me, mt, g, o))) return rc;
+    if (g->n_apps > 0 && (!out || !g->rows || !g->budgets || !g->sm_clock || !g->mem_clock ||
+                          (g->n_cat > 0 && (!g->cat_t || !g->cat_cols)))) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null input array");
+    }
+    if (g->n_apps == 0) return GD_OK;
+    const int64_t A = g->n_apps, R = g->n_records, C = g->n_clocks;
+    for (int64_t c = 0; c < C; ++c) {
+        if (g->sm_clock[c] <= 0 || g->mem_clock[c] <= 0) {
+            return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: clock frequencies must be positive");
+        }
+    }
+    for (int32_t k = 0; k < g->n_cat; ++k) {
+        if (g->cat_cols[k] < 0 || g->cat_cols[k] >= g->n_cols) {
+            return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: categorical column out of range");
+        }
+    }
+    if (g->rec_of_clock) {
+        for (int64_t i = 0; i < A * C; ++i) {
+            if (g->rec_of_clock[i] < 0 || g->rec_of_clock[i] >= R) {
+                return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: record index out of range");
+            }
+        }
+    }
+    Scratch s{ctx->stream};
+    const size_t i_rows = s.add(static_cast<size_t>(R) * g->n_cols * sizeof(double));
+    const size_t i_cat = s.add(static_cast<size_t>(R) * g->n_cat * sizeof(double));
+    const size_t i_catc = s.add(static_cast<size_t>(g->n_cat) * sizeof(int32_t));
+    const size_t i_rec = s.add(g->rec_of_clock ? static_cast<size_t>(A) * C * sizeof(int32_t) : 0);
+    const size_t i_sm = s.add(static_cast<size_t>(C) * sizeof(int32_t));
+    const size_t i_mem = s.add(static_cast<size_t>(C) * sizeof(int32_t));
+    const size_t i_bud = s.add(static_cast<size_t>(A) * sizeof(double));
+    const size_t i_out = s.add(static_cast<size_t>(A) * sizeof(gd_decision));
+    const size_t i_e = s.add(e_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
+    const size_t i_t = s.add(t_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
+    const size_t i_rt = s.add(g->rec_of_clock ? static_cast<size_t>(R) * g->n_cols * sizeof(double) : 0);
+    GD_CUDA(s.alloc(), "cudaMallocAsync");
+    auto h2d = [&](size_t i, const void* src) -> cudaError_t {
+        if (!s.pieces[i].second) return cudaSuccess;
+        return cudaMemcpyAsync(s.ptr(i), src, s.pieces[i].second, cudaMemcpyHostToDevice, ctx->stream);
+    };
+    GD_CUDA(h2d(i_rows, g->rows), "H2D rows");
+    GD_CUDA(h2d(i_cat, g->cat_t), "H2D cat_t");
+    GD_CUDA(h2d(i_catc, g->cat_cols), "H2D cat_cols");
+    GD_CUDA(h2d(i_rec, g->rec_of_clock), "H2D rec_of_clock");
+    GD_CUDA(h2d(i_sm, g->sm_clock), "H2D sm");
+    GD_CUDA(h2d(i_mem, g->mem_clock), "H2D mem");
+    GD_CUDA(h2d(i_bud, g->budgets), "H2D budgets");
+    gd_grid dg = *g;
+    dg.rows = static_cast<double*>(s.ptr(i_rows));
+    dg.cat_t = static_cast<double*>(s.ptr(i_cat));
+    dg.cat_cols = static_cast<int32_t*>(s.ptr(i_catc));
+    dg.rec_of_clock = static_cast<int32_t*>(s.ptr(i_rec));
+    dg.sm_clock = static_cast<int32_t*>(s.ptr(i_sm));
+    dg.mem_clock = static_cast<int32_t*>(s.ptr(i_mem));
+    dg.budgets = static_cast<double*>(s.ptr(i_bud));
+    const double* rows_t = nullptr;
+    if (g->rec_of_clock) {
+        rows_t = static_cast<double*>(s.ptr(i_rt));
+        int e = gd::launch_build_rows_t(dg.rows, dg.cat_t, dg.cat_cols, dg.n_cat, R, dg.n_cols,
+                                        const_cast<double*>(rows_t), ctx->stream);
+        ++ctx->launches;
+        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
+    }
+    rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
+                   static_cast<double*>(s.ptr(i_t)), rows_t);
+    if (rc) return rc;
+    GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_out), static_cast<size_t>(A) * sizeof(gd_decision), cudaMemcpyDeviceToHost,
+                            ctx->stream),
+            "D2H decisions");
+    if (e_out) {
+        GD_CUDA(cudaMemcpyAsync(e_out, s.ptr(i_e), static_cast<size_t>(A) * C * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream),
+                "D2H energy");
+    }
+    if (t_out) {
+        GD_CUDA(cudaMemcpyAsync(t_out, s.ptr(i_t), static_cast<size_t>(A) * C * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream),
+                "D2H time");
+    }
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
+    return GD_OK;
+}
+
+int gd_select(gd_ctx* ctx, const double* energy, const double* time, int64_t n_apps, const int32_t* sm_clock,
+              int32_t n_clocks, const double* budgets, const gd_select_opts* o, gd_decision* out) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if (!o || n_apps < 0 || n_clocks <= 0 || n_clocks > gd::kMaxClocks ||
+        (n_apps > 0 && (!energy || !time || !sm_clock || !budgets || !out))) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "gd_select: bad arguments");
+    }
+    if (n_apps == 0) return GD_OK;
+    const int64_t A = n_apps, C = n_clocks;
+    Scratch s{ctx->stream};
+    const size_t i_e = s.add(static_cast<size_t>(A) * C * sizeof(double));
+    const size_t i_t = s.add(static_cast<size_t>(A) * C * sizeof(double));
+    const size_t i_sm = s.add(static_cast<size_t>(C) * sizeof(int32_t));
+    const size_t i_b = s.add(static_cast<size_t>(A) * sizeof(double));
+    const size_t i_o = s.add(static_cast<size_t>(A) * sizeof(gd_decision));
+    GD_CUDA(s.alloc(), "cudaMallocAsync");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_e), energy, s.pieces[i_e].second, cudaMemcpyHostToDevice, ctx->stream), "H2D E");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_t), time, s.pieces[i_t].second, cudaMemcpyHostToDevice, ctx->stream), "H2D T");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_sm), sm_clock, s.pieces[i_sm].second, cudaMemcpyHostToDevice, ctx->stream), "H2D sm");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_b), budgets, s.pieces[i_b].second, cudaMemcpyHostToDevice, ctx->stream), "H2D b");
+    gd::SelectParams p{};
+    p.energy = static_cast<double*>(s.ptr(i_e));
+    p.time = static_cast<double*>(s.ptr(i_t));
+    p.sm = static_cast<int32_t*>(s.ptr(i_sm));
+    p.budgets = static_cast<double*>(s.ptr(i_b));
+    p.out = static_cast<gd_decision*>(s.ptr(i_o));
+    p.n_apps = A;
+    p.n_clocks = n_clocks;
+    p.mode = o->mode;
+    p.objective = o->objective;
+    p.best_effort = o->best_effort;
+    int e = gd::launch_select(p, ctx->sm_count, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "select kernel launch");
+    GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_o), s.pieces[i_o].second, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "select sync");
+    return GD_OK;
+}
+
+int gd_microbench_dadd(gd_ctx* ctx, double* adds_per_second) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if (!adds_per_second) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_microbench_dadd: null out");
+    const int blocks = ctx->sm_count * 8, iters = 1 << 14;
+    double* scratch = nullptr;
+    GD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), blocks * sizeof(double), ctx->stream), "malloc");
+    cudaEvent_t a, b;
+    GD_CUDA(cudaEventCreate(&a), "event");
+    GD_CUDA(cudaEventCreate(&b), "event");
+    gd::launch_dadd_probe(scratch, blocks, iters, ctx->stream);  // warm-up
+    GD_CUDA(cudaEventRecord(a, ctx->stream), "record");
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) gd::launch_dadd_probe(scratch, blocks, iters, ctx->stream);
+    GD_CUDA(cudaEventRecord(b, ctx->stream), "record");
+    ctx->launches += reps + 1;
+    GD_CUDA(cudaEventSynchronize(b), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFreeAsync(scratch, ctx->stream);
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "sync");
+    const double adds = static_cast<double>(blocks) * 256.0 * 8.0 * iters * reps;
+    *adds_per_second = adds / (ms * 1e-3);
+    return GD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// gd_device.cuh -- device-side data layout shared by the sm_100a kernels.
+//
+// Packed ensemble node (16 bytes, one LDG.128 per visited node):
+//   internal: v = threshold (exact double), feat = column, aux = global index
+//             of the left child; the right child is aux + 1 (the packer
+//             re-lays every tree out breadth-first so siblings are adjacent).
+//   leaf:     feat = -1, v = leaf_value, aux = the leaf's ORIGINAL tree-local
+//             node index (what GbtTree::predict_row's `idx` ends on,
+//             models.cpp:71-78) so leaf ids come out in the caller's numbering.
+#pragma once
+
+#include <cstdint>
+
+#include "gdvfs.h"
+
+namespace gd {
+
+struct __align__(16) PNode {
+    double v;
+    int32_t feat;
+    int32_t aux;
+};
+static_assert(sizeof(PNode) == 16, "PNode must stay 16 bytes");
+
+// Everything the fused grid kernel needs, passed as one __grid_constant__.
+struct GridParams {
+    const PNode* e_nodes;
+    const int32_t* e_roots;
+    const PNode* t_nodes;
+    const int32_t* t_roots;
+    double e_base, e_lr, t_base, t_lr;
+    int32_t e_trees, t_trees;
+
+    const double* rows;    // [n_records, n_cols] energy-encoded
+    const double* rows_t;  // [n_records, n_cols] time-encoded (general mode only)
+    const double* cat_t;   // [n_records, n_cat]
+    const int32_t* cat_cols;
+    const int32_t* rec_of_clock;  // [n_apps, n_clocks] or null
+    const int32_t* sm;
+    const int32_t* mem;
+    const double* budgets;
+    gd_decision* out;
+    double* e_out;
+    double* t_out;
+    int64_t n_apps;
+    int32_t n_cols, n_cat, n_clocks, sm_col, mem_col;
+    int32_t mode, objective, best_effort;
+};
+
+struct SelectParams {
+    const double* energy;
+    const double* time;
+    const int32_t* sm;
+    const double* budgets;
+    gd_decision* out;
+    int64_t n_apps;
+    int32_t n_clocks;
+    int32_t mode, objective, best_effort;
+};
+
+// Launchers (gd_kernels.cu).  All enqueue on `stream` and return the
+// cudaError_t of the launch.
+int launch_predict_gbt(const PNode* nodes, const int32_t* roots, int32_t n_trees, double base, double lr,
+                       int clamp, const double* rows, int64_t n_rows, int32_t n_cols, double* out,
+                       int32_t* leaf_ids, int sm_count, void* stream);
+int launch_predict_linear(const double* coef, double intercept, int clamp, const double* rows, int64_t n_rows,
+                          int32_t n_cols, double* out, int sm_count, void* stream);
+int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* cat_cols, int32_t n_cat,
+                        int64_t n_records, int32_t n_cols, double* rows_t, void* stream);
+int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream);
+int launch_select(const SelectParams& p, int sm_count, void* stream);
+int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
+
+// Largest clock catalog the fused kernels take (32 lanes x 16 clocks).
+constexpr int kMaxClocks = 512;
+constexpr int kMaxCols = 1024;
+
+}  // namespace gd

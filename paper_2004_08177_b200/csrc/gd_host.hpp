@@ -1,0 +1,62 @@
+// gd_host.hpp -- host-side runtime objects behind the C ABI (include/gdvfs.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "gd_device.cuh"
+#include "gdvfs.h"
+
+struct gd_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+};
+
+struct gd_model {
+    gd_ctx* ctx = nullptr;
+    int32_t kind = GD_KIND_GBT;
+    int32_t target = GD_TARGET_ENERGY;
+    int32_t n_cols = 0;
+    int32_t max_depth = 0;
+    double base = 0.0;  // GBT base_prediction or linear intercept
+    double lr = 0.0;
+    // Host copy in the caller's node numbering (export / leaf-id meaning).
+    std::vector<int64_t> offsets;
+    std::vector<int32_t> feature, left, right;
+    std::vector<double> threshold, leaf;
+    std::vector<double> coef;
+    std::vector<std::string> columns;  // from a model file; empty when uploaded
+    // Device copy.
+    gd::PNode* d_nodes = nullptr;
+    int32_t* d_roots = nullptr;
+    double* d_coef = nullptr;
+    int64_t packed_nodes = 0;
+
+    int32_t n_trees() const { return offsets.empty() ? 0 : static_cast<int32_t>(offsets.size() - 1); }
+};
+
+namespace gdh {
+
+int set_error(int code, const std::string& msg);
+int cuda_error(cudaError_t e, const char* where);
+
+// Packer: validate the trees and lay them out breadth-first with adjacent
+// children (gd_pack.cpp).
+int pack_forest(const gd_forest_view& f, int32_t n_cols, std::vector<gd::PNode>& nodes,
+                std::vector<int32_t>& roots, int32_t& max_depth);
+
+// "gpudvfs-model 1" parser (gd_model_io.cpp); fills the host fields of `m`.
+int parse_model_file(const char* path, gd_model& m);
+
+// Host selection for one job at a dynamic budget (gd_edf.cpp); the same
+// rules as the device epilogue.
+void select_one(const double* E, const double* T, const int32_t* sm, int32_t n, double budget,
+                const gd_select_opts& o, gd_decision& out);
+
+}  // namespace gdh

@@ -1,0 +1,301 @@
+"""Seeded synthetic inputs for the (app x clock) evaluation path.
+
+Everything here is deterministic in its seed and shared by the parity tests,
+``bench.py`` and ``__graft_entry__.smoke()``, so the GPU path and the CPU
+reference always consume identical bytes.
+
+* Clock catalogs in ``clock_catalog`` order (mem asc, sm asc;
+  reference core.cpp:177-184): the P100 62-clock grid
+  (synthdata.cpp:271-287), the GTX-980-style 267-pair grid
+  (tests/test_core.cpp:96-108) and a B200-style 200-clock grid.
+* Ensembles in the reference's ``GbtTree`` node format (models.hpp:35-43):
+  ``feature`` (-1 = leaf), ``threshold``, tree-local ``left``/``right``,
+  ``leaf_value``, nodes in preorder as ``load_model`` produces them
+  (models.cpp:581-607).  Thresholds are midpoints of two adjacent sorted pool
+  values, like the trainer's split points (models.cpp:281).
+* App rows with the reference's 50-column schema positions: categorical
+  columns 0 (``double_precision_fu_utilisation``) and 3
+  (``dram_utilisation``), ``mem_clock`` at 25 and ``sm_clock`` at 42
+  (names sorted per ingest.cpp:21-34).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Optional
+
+import numpy as np
+
+N_COLS = 50
+CAT_COLS = (0, 3)
+MEM_COL = 25
+SM_COL = 42
+
+
+def _lround(x: float) -> int:
+    """std::lround for the non-negative values used here (half away from zero)."""
+    return int(math.floor(x + 0.5))
+
+
+def _sorted_catalog(pairs):
+    pairs = sorted(set(pairs), key=lambda p: (p[1], p[0]))
+    sm = np.array([p[0] for p in pairs], dtype=np.int32)
+    mem = np.array([p[1] for p in pairs], dtype=np.int32)
+    return sm, mem
+
+
+def catalog_p100():
+    """synthdata.cpp:271-287: 62 sm clocks in [544, 1328] at mem 715, i=50 forced to 1189."""
+    pairs = []
+    for i in range(62):
+        sm = _lround(544.0 + (1328.0 - 544.0) * i / 61.0)
+        if i == 50:
+            sm = 1189
+        pairs.append((sm, 715))
+    return _sorted_catalog(pairs)
+
+
+def catalog_gtx980():
+    """tests/test_core.cpp:96-108: mem {3505, 2600, 810} x 87 sm clocks + mem 405 x 6 = 267."""
+    pairs = [(135 + 15 * i, mem) for mem in (3505, 2600, 810) for i in range(87)]
+    pairs += [(135 + 15 * i, 405) for i in range(6)]
+    return _sorted_catalog(pairs)
+
+
+def catalog_b200(n: int = 200):
+    """B200-style grid: mem 3996 MHz x n sm clocks lround-spaced over [510, 1965] MHz."""
+    pairs = [(_lround(510.0 + (1965.0 - 510.0) * i / (n - 1)), 3996) for i in range(n)]
+    return _sorted_catalog(pairs)
+
+
+CATALOGS = {"p100": catalog_p100, "gtx980": catalog_gtx980, "b200": catalog_b200}
+
+
+@dataclasses.dataclass
+class Forest:
+    """One GBT ensemble as flat SoA arrays (models::GbtParams + GbtTree nodes)."""
+
+    tree_offsets: np.ndarray  # int64 [n_trees + 1]
+    feature: np.ndarray  # int32, -1 = leaf
+    threshold: np.ndarray  # float64
+    left: np.ndarray  # int32, tree-local
+    right: np.ndarray  # int32, tree-local
+    leaf_value: np.ndarray  # float64
+    base: float
+    learning_rate: float
+    target: int  # 0 energy (clamped at 0), 1 time
+    n_cols: int
+
+    @property
+    def n_trees(self) -> int:
+        return int(self.tree_offsets.shape[0] - 1)
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.feature.shape[0])
+
+
+@dataclasses.dataclass
+class GridInputs:
+    """Per-app rows (energy encoding) + time-encoded categorical values."""
+
+    rows: np.ndarray  # float64 [n_records, n_cols]
+    cat_t: np.ndarray  # float64 [n_records, n_cat]
+    cat_cols: np.ndarray  # int32 [n_cat]
+    sm: np.ndarray  # int32 [C]
+    mem: np.ndarray  # int32 [C]
+    sm_col: int
+    mem_col: int
+    rec_of_clock: Optional[np.ndarray] = None  # int32 [A, C] or None (record = app)
+
+    @property
+    def n_apps(self) -> int:
+        if self.rec_of_clock is not None:
+            return int(self.rec_of_clock.shape[0])
+        return int(self.rows.shape[0])
+
+    @property
+    def n_clocks(self) -> int:
+        return int(self.sm.shape[0])
+
+
+def _preorder_perm(depth: int) -> np.ndarray:
+    """Level-order index -> preorder index for a complete binary tree of `depth`."""
+    n = (1 << (depth + 1)) - 1
+    perm = np.empty(n, dtype=np.int64)
+    counter = 0
+    stack = [0]
+    while stack:
+        i = stack.pop()
+        perm[i] = counter
+        counter += 1
+        l = 2 * i + 1
+        if l < n:
+            stack.append(l + 1)
+            stack.append(l)
+    return perm
+
+
+class _ColumnModel:
+    """Per-column value distributions (magnitudes 1e-2 .. 1e9, like the
+    reference's counters) plus categorical level encodings per target."""
+
+    def __init__(self, rng: np.random.Generator, n_cols: int, cat_cols, sm, mem, sm_col, mem_col):
+        self.n_cols = n_cols
+        self.cat_cols = tuple(cat_cols)
+        self.sm_col, self.mem_col = sm_col, mem_col
+        self.scale = 10.0 ** rng.uniform(-2.0, 9.0, size=n_cols)
+        # four levels (none/low/mid/high) -> encoded values per target
+        self.levels_e = np.sort(rng.uniform(20.0, 400.0, size=(len(self.cat_cols), 4)), axis=1)
+        self.levels_t = np.sort(rng.uniform(0.5, 12.0, size=(len(self.cat_cols), 4)), axis=1)
+        self.sm_vals = np.unique(sm).astype(np.float64)
+        self.mem_vals = np.unique(mem).astype(np.float64)
+        self.pool = self.scale[None, :] * np.exp(rng.uniform(-1.0, 1.0, size=(256, n_cols)))
+        self.pool.sort(axis=0)
+
+    def thresholds(self, rng: np.random.Generator, feat: np.ndarray, target: int) -> np.ndarray:
+        thr = np.empty(feat.shape, dtype=np.float64)
+        k = rng.integers(0, 255, size=feat.shape)
+        thr[:] = 0.5 * (self.pool[k, feat] + self.pool[k + 1, feat])
+        for ci, c in enumerate(self.cat_cols):
+            m = feat == c
+            lv = self.levels_e[ci] if target == 0 else self.levels_t[ci]
+            j = rng.integers(0, 3, size=int(m.sum()))
+            thr[m] = 0.5 * (lv[j] + lv[j + 1])
+        for col, vals in ((self.sm_col, self.sm_vals), (self.mem_col, self.mem_vals)):
+            m = feat == col
+            if not m.any():
+                continue
+            if len(vals) < 2:
+                thr[m] = vals[0] + 0.5
+                continue
+            j = rng.integers(0, len(vals) - 1, size=int(m.sum()))
+            thr[m] = 0.5 * (vals[j] + vals[j + 1])
+        return thr
+
+
+def make_forest(cols: _ColumnModel, n_trees: int, depth: int, target: int, seed: int,
+                w_clk: float = 0.04, leaf_prob: float = 0.0) -> Forest:
+    """Random ensemble in reference node format.
+
+    Complete trees of `depth` (preorder ids) when leaf_prob == 0; otherwise
+    each internal node below the root turns into a leaf with probability
+    `leaf_prob` (irregular trees, explicit children, still preorder).
+    A fraction `w_clk` of split features are the clock columns.
+    """
+    rng = np.random.default_rng(seed)
+    base = 180.0 if target == 0 else 6.0
+    scale = 120.0 if target == 0 else 4.0
+    non_clock = np.array([c for c in range(cols.n_cols) if c not in (cols.sm_col, cols.mem_col)])
+    if leaf_prob <= 0.0:
+        n_int = (1 << depth) - 1
+        n = (1 << (depth + 1)) - 1
+        perm = _preorder_perm(depth)
+        feat_lv = non_clock[rng.integers(0, len(non_clock), size=(n_trees, n_int))]
+        clk = rng.random(size=(n_trees, n_int)) < w_clk
+        which = rng.random(size=(n_trees, n_int)) < 0.5
+        feat_lv = np.where(clk, np.where(which, cols.sm_col, cols.mem_col), feat_lv).astype(np.int32)
+        thr_lv = cols.thresholds(rng, feat_lv, target)
+        leaf_lv = rng.uniform(-1.0, 1.0, size=(n_trees, n - n_int)) * scale
+        feature = np.full((n_trees, n), -1, dtype=np.int32)
+        threshold = np.zeros((n_trees, n), dtype=np.float64)
+        left = np.full((n_trees, n), -1, dtype=np.int32)
+        right = np.full((n_trees, n), -1, dtype=np.int32)
+        leaf = np.zeros((n_trees, n), dtype=np.float64)
+        lv = np.arange(n)
+        pi = perm[lv[:n_int]]
+        feature[:, pi] = feat_lv
+        threshold[:, pi] = thr_lv
+        left[:, pi] = perm[2 * lv[:n_int] + 1]
+        right[:, pi] = perm[2 * lv[:n_int] + 2]
+        leaf[:, perm[lv[n_int:]]] = leaf_lv
+        offsets = np.arange(n_trees + 1, dtype=np.int64) * n
+        return Forest(offsets, feature.ravel(), threshold.ravel(), left.ravel(), right.ravel(),
+                      leaf.ravel(), base, 0.1, target, cols.n_cols)
+
+    feats, thrs, lefts, rights, leaves, offsets = [], [], [], [], [], [0]
+    for _ in range(n_trees):
+        f_t, th_t, l_t, r_t, v_t = [], [], [], [], []
+
+        def build(d):
+            idx = len(f_t)
+            f_t.append(-1); th_t.append(0.0); l_t.append(-1); r_t.append(-1); v_t.append(0.0)
+            if d == depth or (d > 0 and rng.random() < leaf_prob):
+                v_t[idx] = float(rng.uniform(-1.0, 1.0) * scale)
+                return idx
+            if rng.random() < w_clk:
+                f = cols.sm_col if rng.random() < 0.5 else cols.mem_col
+            else:
+                f = int(non_clock[rng.integers(0, len(non_clock))])
+            f_t[idx] = f
+            th_t[idx] = float(cols.thresholds(rng, np.array([f]), target)[0])
+            l_t[idx] = build(d + 1)
+            r_t[idx] = build(d + 1)
+            return idx
+
+        build(0)
+        feats += f_t; thrs += th_t; lefts += l_t; rights += r_t; leaves += v_t
+        offsets.append(offsets[-1] + len(f_t))
+    return Forest(np.array(offsets, dtype=np.int64), np.array(feats, dtype=np.int32),
+                  np.array(thrs, dtype=np.float64), np.array(lefts, dtype=np.int32),
+                  np.array(rights, dtype=np.int32), np.array(leaves, dtype=np.float64),
+                  base, 0.1, target, cols.n_cols)
+
+
+def make_rows(cols: _ColumnModel, n_apps: int, seed: int, sm_default: int, mem_default: int):
+    rng = np.random.default_rng(seed)
+    rows = cols.scale[None, :] * np.exp(rng.uniform(-1.0, 1.0, size=(n_apps, cols.n_cols)))
+    cat_t = np.empty((n_apps, len(cols.cat_cols)), dtype=np.float64)
+    for ci, c in enumerate(cols.cat_cols):
+        lvl = rng.integers(0, 4, size=n_apps)
+        rows[:, c] = cols.levels_e[ci][lvl]
+        cat_t[:, ci] = cols.levels_t[ci][lvl]
+    rows[:, cols.sm_col] = float(sm_default)
+    rows[:, cols.mem_col] = float(mem_default)
+    return np.ascontiguousarray(rows), np.ascontiguousarray(cat_t)
+
+
+@dataclasses.dataclass
+class Scenario:
+    name: str
+    energy: Forest
+    time: Forest
+    grid: GridInputs
+    seed: int
+
+
+def make_scenario(name: str, n_apps: int, catalog: str, n_trees: int, depth: int, seed: int = 1234,
+                  w_clk: float = 0.04, leaf_prob: float = 0.0) -> Scenario:
+    """A complete synthetic (apps, catalog, E/T ensembles) configuration."""
+    sm, mem = CATALOGS[catalog]()
+    rng = np.random.default_rng(seed)
+    cols = _ColumnModel(rng, N_COLS, CAT_COLS, sm, mem, SM_COL, MEM_COL)
+    fe = make_forest(cols, n_trees, depth, 0, seed + 1, w_clk, leaf_prob)
+    ft = make_forest(cols, n_trees, depth, 1, seed + 2, w_clk, leaf_prob)
+    rows, cat_t = make_rows(cols, n_apps, seed + 3, int(sm[-1]), int(mem[-1]))
+    grid = GridInputs(rows, cat_t, np.array(CAT_COLS, dtype=np.int32), sm, mem, SM_COL, MEM_COL)
+    return Scenario(name, fe, ft, grid, seed)
+
+
+def deadlines_from_times(times: np.ndarray, seed: int, infeasible_frac: float = 0.05) -> np.ndarray:
+    """Per-app relative deadline: a seeded quantile q ~ U(0.1, 0.9) of the app's own
+    predicted times over the grid; `infeasible_frac` of apps
+    get half their minimum time so the rejected / best-effort paths run."""
+    rng = np.random.default_rng(seed)
+    a = times.shape[0]
+    q = rng.uniform(0.1, 0.9, size=a)
+    srt = np.sort(times, axis=1)
+    idx = np.minimum((q * (times.shape[1] - 1)).astype(np.int64), times.shape[1] - 1)
+    dl = srt[np.arange(a), idx].copy()
+    bad = rng.random(size=a) < infeasible_frac
+    dl[bad] = srt[bad, 0] * 0.5
+    return dl
+
+
+# The BASELINE.json configurations.
+CONFIGS = {
+    "c2": dict(n_apps=10_000, catalog="gtx980", n_trees=500, depth=8),
+    "c3": dict(n_apps=1_000_000, catalog="b200", n_trees=1000, depth=10),
+    "c4": dict(n_apps=10_000_000, catalog="gtx980", n_trees=2000, depth=12),
+    "c5": dict(n_apps=64, catalog="gtx980", n_trees=500, depth=8),
+}

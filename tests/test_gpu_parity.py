@@ -1,0 +1,263 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the oracle
+and the reference's golden vectors.  Integer/index results (leaf ids, chosen
+clocks, statuses) must be identical; predictions are compared bit-for-bit
+(the path is exact FP64 -- stricter than north_star's 1e-5 relative bound,
+which tests/test_gpu_parity.py::test_sum_tolerance_statement documents).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_2004_08177_b200 as gd
+from helpers import GOLDEN, bits, c1_combo, c1_small, decisions_equal, golden_forest, parse_model_text, tie_tables
+from paper_2004_08177_b200 import workload as W
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # north_star's bound for summed predictions; we require 0 ulp
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = gd.Context(0)
+    yield c
+    c.close()
+
+
+def opts_of(mode, budget, obj, be):
+    return gd.SchedulerOptions(mode=["text", "literal"][mode], budget=["remaining", "full"][budget],
+                               objective=["energy", "power"][obj], best_effort_fallback=bool(be))
+
+
+# ---- K1 predict_rows ---------------------------------------------------------
+
+@pytest.mark.parametrize("key", ["complete_0", "complete_1", "irregular_0", "irregular_1", "neg"])
+def test_k1_predict_matches_reference_golden(ctx, key):
+    npz = np.load(GOLDEN / "predict.npz")
+    f = golden_forest(npz, key, 1 if key.endswith("_1") else 0)
+    m = gd.Model.from_forest(f, ctx)
+    got, ids = m.predict(npz[f"{key}_rows"], leaf_ids=True)
+    assert np.array_equal(bits(got), bits(npz[f"{key}_pred"]))
+    want_p, want_ids = O.oracle_predict(f, npz[f"{key}_rows"], leaf_ids=True)
+    assert np.array_equal(ids, want_ids)
+
+
+@pytest.mark.parametrize("leaf_prob,depth,trees", [(0.0, 8, 67), (0.35, 10, 40), (0.0, 1, 5), (0.2, 12, 33)])
+def test_k1_predict_leaf_ids_vs_oracle(ctx, leaf_prob, depth, trees):
+    sc = W.make_scenario("k1", 50, "gtx980", trees, depth, seed=depth, w_clk=0.1, leaf_prob=leaf_prob)
+    rows = np.repeat(sc.grid.rows, 7, axis=0)
+    rows[:, W.SM_COL] = np.resize(sc.grid.sm, rows.shape[0])
+    for f in (sc.energy, sc.time):
+        m = gd.Model.from_forest(f, ctx)
+        got, ids = m.predict(rows, leaf_ids=True)
+        want, want_ids = O.oracle_predict(f, rows, leaf_ids=True)
+        assert np.array_equal(bits(got), bits(want))
+        assert np.array_equal(ids, want_ids)
+
+
+def test_k1_model_file_and_c1_models(ctx):
+    npz = np.load(GOLDEN / "model_file_pred.npz")
+    m = gd.Model.load_file(GOLDEN / "model_time_small.txt", ctx)
+    assert np.array_equal(bits(m.predict(npz["rows"])), bits(npz["pred"]))
+    s = c1_small()
+    me = gd.Model.load_file(s["model_energy"], ctx)
+    rows = s["rows"]
+    got, ids = me.predict(rows, leaf_ids=True)
+    want, want_ids = O.oracle_predict(s["fe"], rows, leaf_ids=True)
+    assert np.array_equal(bits(got), bits(want)) and np.array_equal(ids, want_ids)
+
+
+def test_k1_edge_cases(ctx):
+    f = W.make_scenario("e", 3, "p100", 5, 3, seed=2).time
+    m = gd.Model.from_forest(f, ctx)
+    assert m.predict(np.zeros((0, W.N_COLS))).shape == (0,)
+    with pytest.raises(ValueError, match="column mismatch"):
+        m.predict(np.zeros((2, W.N_COLS - 1)))
+    # zero trees: base prediction only (models.cpp:370-377 with an empty loop)
+    z = W.Forest(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0), np.zeros(0, np.int32),
+                 np.zeros(0, np.int32), np.zeros(0), 3.5, 0.1, 1, W.N_COLS)
+    out = gd.Model.from_forest(z, ctx).predict(np.ones((4, W.N_COLS)))
+    assert np.all(out == 3.5)
+    # a single-leaf tree
+    one = W.Forest(np.array([0, 1], np.int64), np.array([-1], np.int32), np.zeros(1), np.array([-1], np.int32),
+                   np.array([-1], np.int32), np.array([2.0]), 1.0, 0.5, 1, W.N_COLS)
+    assert np.all(gd.Model.from_forest(one, ctx).predict(np.ones((3, W.N_COLS))) == 2.0)
+
+
+def test_k1_linear(ctx):
+    rng = np.random.default_rng(0)
+    coef = rng.normal(size=W.N_COLS)
+    rows = rng.normal(size=(300, W.N_COLS)) * 10
+    for target in (0, 1):
+        m = gd.Model.linear(coef, -0.25, target=target, ctx=ctx)
+        got = m.predict(rows)
+        want = O.oracle_predict_linear(coef, -0.25, int(target == 0), rows)
+        assert np.array_equal(bits(got), bits(want))
+
+
+# ---- K2+K3 fused grid --------------------------------------------------------
+
+SCENARIOS = {
+    "c2_shape": dict(n_apps=300, catalog="gtx980", n_trees=60, depth=8, w_clk=0.04),
+    "stress_clk": dict(n_apps=200, catalog="gtx980", n_trees=40, depth=8, w_clk=0.25),
+    "fallback": dict(n_apps=64, catalog="b200", n_trees=35, depth=10, w_clk=0.6),
+    "irregular": dict(n_apps=150, catalog="p100", n_trees=70, depth=10, w_clk=0.05, leaf_prob=0.3),
+    "tiny_grid": dict(n_apps=33, catalog="p100", n_trees=3, depth=2, w_clk=0.5),
+}
+
+
+def scenario(name):
+    kw = dict(SCENARIOS[name])
+    return W.make_scenario(name, kw.pop("n_apps"), kw.pop("catalog"), kw.pop("n_trees"), kw.pop("depth"), seed=11,
+                           **kw)
+
+
+@pytest.mark.parametrize("name", list(SCENARIOS))
+def test_k2_grid_predictions_and_decisions_vs_oracle(ctx, name):
+    sc = scenario(name)
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, e0, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=5)
+    for combo in itertools.product((0, 1), (1,), (0, 1), (0, 1)):
+        mode, _, obj, be = combo
+        want, we, wt = O.oracle_grid(sc.energy, sc.time, sc.grid, budgets, mode, obj, be)
+        got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, opts_of(*combo), return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we)), (name, combo)
+        assert np.array_equal(bits(gt), bits(wt)), (name, combo)
+        assert decisions_equal(got, want), (name, combo)
+
+
+def test_k2_general_mode_c1_golden(ctx):
+    # Per-clock records (nearest-record substitution, scheduler.cpp:341-359):
+    # predictions must equal the reference's ClockPredictor outputs bit for bit.
+    s = c1_small()
+    me, mt = gd.Model.load_file(s["model_energy"], ctx), gd.Model.load_file(s["model_time"], ctx)
+    got, e, t = gd.grid_select(me, mt, s["grid"], s["deadline"], gd.SchedulerOptions(budget="full"),
+                               return_predictions=True)
+    assert np.array_equal(bits(e), bits(s["pred_energy"]))
+    assert np.array_equal(bits(t), bits(s["pred_time"]))
+    want, _, _ = O.oracle_grid(s["fe"], s["ft"], s["grid"], s["deadline"])
+    assert decisions_equal(got, want)
+
+
+@pytest.mark.parametrize("tag", ["".join(map(str, c)) for c in itertools.product((0, 1), repeat=4)])
+def test_end_to_end_schedule_c1_golden(ctx, tag):
+    # GPU predictions -> host EDF loop == the reference's schedule_d_dvfs.
+    s = c1_small()
+    me, mt = gd.Model.load_file(s["model_energy"], ctx), gd.Model.load_file(s["model_time"], ctx)
+    _, e, t = gd.grid_select(me, mt, s["grid"], s["deadline"], return_predictions=True)
+    mode, budget, obj, be = (int(c) for c in tag)
+    want, want_order = c1_combo(s, tag)
+    got, order = gd.schedule_d_dvfs(s["jobs"], e, t, s["sm"], s["exec"], opts_of(mode, budget, obj, be))
+    assert decisions_equal(got, want) and np.array_equal(order, want_order)
+
+
+def test_c1_full_scale_live_reference(ctx, tmp_path):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    s = O.ref_c1_scenario(tmp_path, seed=7, iters=100, depth=10, n_jobs=100)
+    me, mt = gd.Model.load_file(s["model_energy"], ctx), gd.Model.load_file(s["model_time"], ctx)
+    g = W.GridInputs(s["rows"], s["cat_t"], s["cat_cols"], s["sm"], s["mem"], s["sm_col"], s["mem_col"],
+                     s["rec_of_clock"])
+    _, e, t = gd.grid_select(me, mt, g, s["deadline"], return_predictions=True)
+    assert np.array_equal(bits(e), bits(s["pred_energy"])) and np.array_equal(bits(t), bits(s["pred_time"]))
+    jobs = np.zeros(s["n_jobs"], O.JOB_DTYPE)
+    jobs["arrival_s"], jobs["deadline_s"] = s["arrival"], s["deadline"]
+    jobs["app_rank"] = jobs["app_index"] = np.arange(s["n_jobs"])
+    got, order = gd.schedule_d_dvfs(jobs, e, t, s["sm"], s["exec"])
+    assert decisions_equal(got, s["decisions"]) and np.array_equal(order, s["order"])
+
+
+def test_k2_edge_cases(ctx):
+    sc = scenario("tiny_grid")
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    # empty batch
+    g0 = W.GridInputs(sc.grid.rows[:0], sc.grid.cat_t[:0], sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, W.SM_COL,
+                      W.MEM_COL)
+    assert gd.grid_select(me, mt, g0, np.zeros(0)).shape == (0,)
+    # single-clock catalog; all infeasible with and without best effort
+    g1 = W.GridInputs(sc.grid.rows, sc.grid.cat_t, sc.grid.cat_cols, sc.grid.sm[:1], sc.grid.mem[:1], W.SM_COL,
+                      W.MEM_COL)
+    for be in (0, 1):
+        want, _, _ = O.oracle_grid(sc.energy, sc.time, g1, np.full(sc.grid.n_apps, -1.0), 0, 0, be)
+        got = gd.grid_select(me, mt, g1, np.full(sc.grid.n_apps, -1.0), opts_of(0, 1, 0, be))
+        assert decisions_equal(got, want)
+        assert np.all(got["status"] == (0 if be else 1))
+    # budget exactly equal to a candidate's time is feasible (T > budget skips)
+    _, _, t = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
+    b = t[:, 5].copy()
+    want, _, _ = O.oracle_grid(sc.energy, sc.time, sc.grid, b)
+    assert decisions_equal(gd.grid_select(me, mt, sc.grid, b), want)
+    assert np.all(want["status"] == 0)
+    # wrong model roles / column counts fail loudly
+    with pytest.raises(ValueError):
+        gd.grid_select(mt, me, sc.grid, b)
+    bad = W.GridInputs(sc.grid.rows[:, :10], sc.grid.cat_t, sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, 3, 4)
+    with pytest.raises(ValueError):
+        gd.grid_select(me, mt, bad, b)
+
+
+# ---- K3 select alone -----------------------------------------------------------
+
+@pytest.mark.parametrize("seed", range(4))
+def test_k3_acceptance1_truth_golden(ctx, seed):
+    # SPEC.md:599 acceptance #1: text selection on the truth tables == oracle_per_job.
+    npz = np.load(GOLDEN / "truth.npz")
+    got = gd.select(npz[f"s{seed}_E"], npz[f"s{seed}_T"], npz["sm"], npz[f"s{seed}_deadline"], ctx=ctx)
+    assert decisions_equal(got, npz[f"s{seed}_decisions"])
+
+
+@pytest.mark.parametrize("n_clocks", [1, 2, 31, 32, 33, 62, 200, 267, 512])
+def test_k3_tie_breaks_vs_oracle(ctx, n_clocks):
+    rng = np.random.default_rng(n_clocks)
+    A = 257
+    E, T = tie_tables(rng, A, n_clocks)
+    sm = np.sort(rng.integers(100, 2000, size=n_clocks)).astype(np.int32)  # duplicates allowed (multi-mem grids)
+    budgets = rng.choice(np.unique(T), size=A) + rng.choice([0.0, -0.1, 0.1], size=A)
+    for combo in itertools.product((0, 1), (1,), (0, 1), (0, 1)):
+        mode, _, obj, be = combo
+        want = O.oracle_select(E, T, sm, budgets, mode, obj, be)
+        got = gd.select(E, T, sm, budgets, opts_of(*combo), ctx=ctx)
+        assert decisions_equal(got, want), combo
+
+
+def test_spec_examples_gpu(ctx):
+    E, T = np.array([[100.0, 150.0]] * 3), np.array([[10.0, 5.0]] * 3)
+    got = gd.select(E, T, np.array([500, 1000], np.int32), np.array([8.0, 12.0, 3.0]), ctx=ctx)
+    assert list(got["clock_index"]) == [1, 0, -1]
+    assert list(got["status"]) == [0, 0, 1]
+
+
+# ---- full-size properties ------------------------------------------------------
+
+def test_c2_full_size_properties(ctx):
+    # BASELINE configs[1] at full size: 10k apps x 267 clocks, 500 trees depth 8.
+    sc = W.make_scenario("c2", **W.CONFIGS["c2"])
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    first, e, t = gd.grid_select(me, mt, sc.grid, np.ones(sc.grid.n_apps), return_predictions=True)
+    budgets = W.deadlines_from_times(t, seed=3)
+    d1, e1, t1 = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
+    d2 = gd.grid_select(me, mt, sc.grid, budgets)
+    assert decisions_equal(d1, d2)  # determinism
+    assert np.array_equal(bits(e1), bits(e)) and np.array_equal(bits(t1), bits(t))
+    # decisions are the selection of the returned tables (K3 consistency)
+    assert decisions_equal(O.oracle_select(e1, t1, sc.grid.sm, budgets), d1)
+    # a seeded sample of apps against the oracle end to end
+    idx = np.random.default_rng(0).choice(sc.grid.n_apps, 24, replace=False)
+    sub = W.GridInputs(sc.grid.rows[idx], sc.grid.cat_t[idx], sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, W.SM_COL,
+                       W.MEM_COL)
+    want, we, wt = O.oracle_grid(sc.energy, sc.time, sub, budgets[idx])
+    assert np.array_equal(bits(e1[idx]), bits(we)) and np.array_equal(bits(t1[idx]), bits(wt))
+    assert decisions_equal(d1[idx], want)
+    # feasibility soundness (SPEC invariant): scheduled => T <= budget
+    ok = (d1["status"] == 0) & (d1["note"] == 0)
+    assert np.all(d1["time_s"][ok] <= budgets[ok])
+    assert 0 < ok.sum() < sc.grid.n_apps
+
+
+def test_sum_tolerance_statement():
+    # The kernels are bit-exact; north_star's 1e-5 relative tolerance is the
+    # documented ceiling and is implied by 0-ulp equality above.
+    assert REL_TOL == 1e-5
