@@ -43,6 +43,7 @@ def parse_args():
     p.add_argument("--config", default="c2")
     p.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of CPU baseline work")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling (use under ncu)")
     return p.parse_args()
 
 
@@ -171,8 +172,29 @@ def run_ours(args, rank, world, local_rank):
     del t_tab
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    sampler = ClockSampler(local_rank, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") \
-        if (ROOT / "gpurun_out").is_dir() else ClockSampler(local_rank, Path(f"/tmp/gd_clocks_r{rank}.csv"))
+    sampler = None
+    if not args.no_clocks:
+        out_dir = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else Path("/tmp")
+        sampler = ClockSampler(local_rank, out_dir / f"clocks_r{rank}.csv")
+    try:
+        return _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_total, lo, hi, ptrs,
+                      out_d, bud_d, budgets, flush, launch, opts, sampler)
+    finally:
+        if sampler is not None and sampler.proc is not None and sampler.proc.poll() is None:
+            sampler.proc.kill()
+
+
+def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_total, lo, hi, ptrs, out_d, bud_d,
+           budgets, flush, launch, opts, sampler):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_08177_b200 as gd
+    from paper_2004_08177_b200 import shard
+    from paper_2004_08177_b200 import workload as W
+
+    A = hi - lo
+    C_, F, K = g.n_clocks, g.rows.shape[1], g.cat_t.shape[1]
 
     def step(timing=None):
         flush.zero_()
@@ -220,7 +242,8 @@ def run_ours(args, rank, world, local_rank):
     h_grid = W.GridInputs(pin(g.rows[lo:hi]), pin(g.cat_t[lo:hi]), pin(g.cat_cols.astype(np.int32)),
                           pin(g.sm.astype(np.int32)), pin(g.mem.astype(np.int32)), g.sm_col, g.mem_col)
     h_bud = pin(budgets)
-    h_out = torch.zeros(A * shard.DECISION_BYTES, dtype=torch.uint8).pin_memory().numpy().view(gd.DECISION_DTYPE)
+    h_out = torch.zeros(A * shard.DECISION_BYTES // 8, dtype=torch.float64).pin_memory().numpy().view(
+        gd.DECISION_DTYPE)
     for _ in range(max(args.warmup, 1)):
         gd.grid_select(me, mt, h_grid, h_bud, opts, out=h_out)
     torch.cuda.synchronize(dev)
@@ -238,7 +261,7 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler is not None else None
 
     # Consistency: the device-resident run and the e2e run agree.
     dev_dec = out_d.cpu().numpy().view(gd.DECISION_DTYPE)

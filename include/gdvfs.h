@@ -80,9 +80,8 @@ typedef struct gd_model_info {
 /* 24-byte per-app decision record (ScheduleDecision minus the Job copy). */
 typedef struct gd_decision {
     int32_t clock_index; /* index into the clock_catalog order, -1 = none */
-    int32_t status;      /* GD_SCHEDULED / GD_REJECTED */
-    int32_t note;        /* GD_NOTE_* */
-    int32_t pad;
+    int16_t status;      /* GD_SCHEDULED / GD_REJECTED */
+    int16_t note;        /* GD_NOTE_* */
     double energy_ws;    /* predicted E of the chosen clock (0 if none) */
     double time_s;       /* predicted T of the chosen clock (0 if none) */
 } gd_decision;

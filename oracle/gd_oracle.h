@@ -40,9 +40,8 @@ typedef struct gdo_forest {
 
 typedef struct gdo_decision {
     int32_t clock_index; /* catalog index, -1 when rejected */
-    int32_t status;      /* 0 scheduled, 1 rejected_infeasible */
-    int32_t note;        /* 0 none, 1 "best_effort", 2 "missing correlated data" */
-    int32_t pad;
+    int16_t status;      /* 0 scheduled, 1 rejected_infeasible */
+    int16_t note;        /* 0 none, 1 "best_effort", 2 "missing correlated data" */
     double energy_ws;
     double time_s;
 } gdo_decision;

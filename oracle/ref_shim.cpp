@@ -46,9 +46,8 @@ struct ForestView {
 
 struct Decision {
     int32_t clock_index;
-    int32_t status;
-    int32_t note;
-    int32_t pad;
+    int16_t status;
+    int16_t note;
     double energy_ws;
     double time_s;
 };

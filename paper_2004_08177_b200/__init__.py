@@ -41,8 +41,9 @@ MODE = {"text": 0, "text_semantics": 0, "literal": 1, "literal_pseudocode": 1}
 OBJECTIVE = {"energy": 0, "power": 1}
 BUDGET = {"remaining": 0, "remaining_time": 0, "full": 1, "full_deadline": 1}
 
-DECISION_DTYPE = np.dtype([("clock_index", "<i4"), ("status", "<i4"), ("note", "<i4"), ("pad", "<i4"),
-                           ("energy_ws", "<f8"), ("time_s", "<f8")])
+DECISION_DTYPE = np.dtype([("clock_index", "<i4"), ("status", "<i2"), ("note", "<i2"), ("energy_ws", "<f8"),
+                           ("time_s", "<f8")])
+assert DECISION_DTYPE.itemsize == 24
 JOB_DTYPE = np.dtype([("arrival_s", "<f8"), ("deadline_s", "<f8"), ("app_rank", "<i8"), ("app_index", "<i4"),
                       ("pad", "<i4")])
 

@@ -250,7 +250,6 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
         d.clock_index = best.idx;
         d.status = best.idx >= 0 ? GD_SCHEDULED : GD_REJECTED;
         d.note = best.idx >= 0 ? note : GD_NOTE_NONE;
-        d.pad = 0;
         d.energy_ws = best.idx >= 0 ? best.e : 0.0;
         d.time_s = best.idx >= 0 ? best.t : 0.0;
         *out = d;

@@ -19,8 +19,9 @@ ORACLE_SO = ORACLE_DIR / "liboracle.so"
 REF_SO = ORACLE_DIR / "_ref" / "libgpudvfs_ref.so"
 REF_SRC = Path("/root/reference/proj")
 
-DECISION_DTYPE = np.dtype([("clock_index", "<i4"), ("status", "<i4"), ("note", "<i4"), ("pad", "<i4"),
-                           ("energy_ws", "<f8"), ("time_s", "<f8")])
+DECISION_DTYPE = np.dtype([("clock_index", "<i4"), ("status", "<i2"), ("note", "<i2"), ("energy_ws", "<f8"),
+                           ("time_s", "<f8")])
+assert DECISION_DTYPE.itemsize == 24
 JOB_DTYPE = np.dtype([("arrival_s", "<f8"), ("deadline_s", "<f8"), ("app_rank", "<i8"), ("app_index", "<i4"),
                       ("pad", "<i4")])
 
