@@ -143,7 +143,11 @@ def run_ours(args, rank, world, local_rank):
     C_, F, K = g.n_clocks, g.rows.shape[1], g.cat_t.shape[1]
 
     ctx = gd.Context(local_rank)
-    stream = torch.cuda.current_stream(dev)
+    # One explicit (non-default) stream for everything: torch's flush kernels,
+    # the CUDA events and our launches (gd_ctx_set_stream(NULL) would mean
+    # "the context's own stream", so the legacy default stream is not used).
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     me = gd.Model.from_forest(sc.energy, ctx)
     mt = gd.Model.from_forest(sc.time, ctx)

@@ -37,6 +37,13 @@ constexpr int kRnCap = 128;          // reduced clock-node slots per warp per 32
 constexpr int kRlCap = 256;          // reduced leaf slots per warp per chunk
 constexpr int kStack = 24;           // DFS stack (>= max depth + 1 for depth <= 23)
 
+// Shared memory of one warp in the partial-evaluation grid kernel:
+// rowE[F] + rowT[F] doubles, val[32] + valr[32] doubles, the residue pool
+// (kRnCap int4 + kRlCap doubles), code[32] ints, 2 counters (16 B padded).
+__host__ __device__ constexpr size_t grid_smem_per_warp(int n_cols) {
+    return 2 * static_cast<size_t>(n_cols) * 8 + 64 * 8 + kRnCap * 16 + kRlCap * 8 + 32 * 4 + 16;
+}
+
 __device__ __forceinline__ void load_node(const PNode* __restrict__ nodes, int32_t n, double& v, int32_t& feat,
                                           int32_t& aux) {
     const int4 q = __ldg(reinterpret_cast<const int4*>(nodes) + n);
@@ -194,7 +201,7 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
     if (mode == GD_MODE_TEXT) {
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-            const int c = lane + 32 * i;
+            const int c = lane * CPL + i;
             if (c < n_clocks && !(T[i] > budget)) {
                 Cand k{objective_value(E[i], T[i], objective), T[i], E[i], smv[i], c};
                 if (text_less(k, best)) best = k;
@@ -208,15 +215,17 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
     } else {
         // scheduler.cpp:86-100: sequential scan in catalog order, DBL_MAX
         // init, bound tightened to each accepted candidate's time.  Every lane
-        // runs the same scan on broadcast values.
+        // runs the same scan on broadcast values (lane l owns clocks
+        // l*CPL .. l*CPL+CPL-1, so lane-major order is catalog order).
         double min_objective = DBL_MAX, max_time = budget;
+        for (int l = 0; l < 32; ++l) {
+            if (l * CPL >= n_clocks) break;
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            for (int l = 0; l < 32; ++l) {
-                const int c = 32 * i + l;
-                if (c >= n_clocks) break;
+            for (int i = 0; i < CPL; ++i) {
+                const int c = l * CPL + i;
                 const double e = __shfl_sync(kFull, E[i], l);
                 const double t = __shfl_sync(kFull, T[i], l);
+                if (c >= n_clocks) continue;
                 const double value = objective_value(e, t, objective);
                 if (value < min_objective && t <= max_time) {
                     min_objective = value;
@@ -232,7 +241,7 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
     if (best.idx < 0 && best_effort) {
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-            const int c = lane + 32 * i;
+            const int c = lane * CPL + i;
             if (c < n_clocks) {
                 Cand k{0.0, T[i], E[i], smv[i], c};
                 if (fast_less(k, best)) best = k;
@@ -284,19 +293,43 @@ struct WarpPool {
     int* counts;   // [0] rn used, [1] rl used
 };
 
-enum : int { kConst = 0, kDag = 1, kFallback = 2 };
+enum : int { kConst = 0, kSingle = 1, kDag = 2, kFallback = 3 };
 
-// Phase 1 for one tree.  Returns kConst (val = leaf), kDag (code = residue
-// root) or kFallback (code = first clock node; pool exhausted).
-__device__ int reduce_tree(const PNode* __restrict__ nodes, int32_t root, const double* row, int sm_col,
-                           int mem_col, const WarpPool& pool, double& val, int& code) {
+__device__ __forceinline__ bool stops(int32_t feat, int sm_col, int mem_col) {
+    return feat < 0 || feat == sm_col || feat == mem_col;
+}
+
+// Two independent row-only walks advanced together (ILP for the two
+// continuations below a clock node).
+__device__ __forceinline__ void walk_row2(const PNode* __restrict__ nodes, int32_t a, int32_t b, const double* row,
+                                          int sm_col, int mem_col, double& va, int32_t& fa, double& vb,
+                                          int32_t& fb) {
+    int32_t xa, xb;
+    load_node(nodes, a, va, fa, xa);
+    load_node(nodes, b, vb, fb, xb);
+    bool da = stops(fa, sm_col, mem_col), db = stops(fb, sm_col, mem_col);
+    while (!(da && db)) {
+        if (!da) a = (row[fa] <= va) ? xa : xa + 1;
+        if (!db) b = (row[fb] <= vb) ? xb : xb + 1;
+        if (!da) {
+            load_node(nodes, a, va, fa, xa);
+            da = stops(fa, sm_col, mem_col);
+        }
+        if (!db) {
+            load_node(nodes, b, vb, fb, xb);
+            db = stops(fb, sm_col, mem_col);
+        }
+    }
+}
+
+// General residue: the clock-only DAG below clock node `first`, built into
+// the warp's pool by an explicit DFS.  Returns kDag (code = residue root) or
+// kFallback (code = first; pool or stack exhausted).
+__device__ __noinline__ int reduce_residue(const PNode* __restrict__ nodes, int32_t first, const double* row,
+                                           int sm_col, int mem_col, const WarpPool& pool, int& code) {
     double v;
     int32_t feat, aux;
-    const int32_t first = walk_row(nodes, root, row, sm_col, mem_col, v, feat, aux);
-    if (feat < 0) {
-        val = v;
-        return kConst;
-    }
+    load_node(nodes, first, v, feat, aux);
     const int r0 = atomicAdd(&pool.counts[0], 1);
     if (r0 >= kRnCap) {
         code = first;
@@ -336,6 +369,33 @@ __device__ int reduce_tree(const PNode* __restrict__ nodes, int32_t root, const 
     return kDag;
 }
 
+// Phase 1 for one tree.  kConst: val = the leaf every candidate reaches.
+// kSingle (the common non-constant case): one clock test separates two
+// leaves -- val/valr = left/right leaf, code = integer threshold, memkind =
+// the test is on mem_clock.  kDag / kFallback: see reduce_residue.
+__device__ __forceinline__ int classify_tree(const PNode* __restrict__ nodes, int32_t root, const double* row,
+                                             int sm_col, int mem_col, const WarpPool& pool, double& val,
+                                             double& valr, int& code, bool& memkind) {
+    double v;
+    int32_t feat, aux;
+    const int32_t first = walk_row(nodes, root, row, sm_col, mem_col, v, feat, aux);
+    if (feat < 0) {
+        val = v;
+        return kConst;
+    }
+    memkind = feat == mem_col;
+    double vl, vr;
+    int32_t fl, fr;
+    walk_row2(nodes, aux, aux + 1, row, sm_col, mem_col, vl, fl, vr, fr);
+    if (fl < 0 && fr < 0) {
+        val = vl;
+        valr = vr;
+        code = thr_to_int(v);
+        return kSingle;
+    }
+    return reduce_residue(nodes, first, row, sm_col, mem_col, pool, code);
+}
+
 __device__ __forceinline__ double eval_dag(const WarpPool& pool, int code, int sm, int mem) {
     while (code >= 0) {
         const int4 r = pool.rn[code];
@@ -368,30 +428,35 @@ struct ModelRef {
 // All trees of one model for one app (partial-evaluation path).
 template <int CPL>
 __device__ __forceinline__ void accumulate_model(const ModelRef m, const double* row, const GridParams& p,
-                                                 const WarpPool& pool, double* chunk_val, int* chunk_code,
-                                                 const int (&smv)[CPL], const int (&memv)[CPL], int lane,
-                                                 double (&acc)[CPL]) {
+                                                 const WarpPool& pool, double* chunk_val, double* chunk_valr,
+                                                 int* chunk_code, const int (&smv)[CPL], const int (&memv)[CPL],
+                                                 int lane, double (&acc)[CPL]) {
     for (int32_t t0 = 0; t0 < m.n_trees; t0 += 32) {
         const int32_t t = t0 + lane;
         int kind = kConst;
+        bool memkind = false;
         if (lane == 0) {
             pool.counts[0] = 0;
             pool.counts[1] = 0;
         }
         __syncwarp();
         if (t < m.n_trees) {
-            double val = 0.0;
+            double val = 0.0, valr = 0.0;
             int code = 0;
-            kind = reduce_tree(m.nodes, __ldg(m.roots + t), row, p.sm_col, p.mem_col, pool, val, code);
+            kind = classify_tree(m.nodes, __ldg(m.roots + t), row, p.sm_col, p.mem_col, pool, val, valr, code,
+                                 memkind);
             chunk_val[lane] = val;
+            chunk_valr[lane] = valr;
             chunk_code[lane] = code;
         }
         const unsigned nonconst = __ballot_sync(kFull, kind != kConst);
+        const unsigned single = __ballot_sync(kFull, kind == kSingle);
+        const unsigned on_mem = __ballot_sync(kFull, kind == kSingle && memkind);
         const unsigned fallback = __ballot_sync(kFull, kind == kFallback);
         __syncwarp();
         const int nt = min(32, m.n_trees - t0);
         if (nonconst == 0u && nt == 32) {
-            // Common case: every tree of the chunk is constant over the grid.
+            // Every tree of the chunk is constant over the grid.
 #pragma unroll 4
             for (int j = 0; j < 32; j += 2) {
                 const double2 vv = *reinterpret_cast<const double2*>(chunk_val + j);
@@ -402,11 +467,23 @@ __device__ __forceinline__ void accumulate_model(const ModelRef m, const double*
             }
         } else {
             for (int j = 0; j < nt; ++j) {
-                if (!((nonconst >> j) & 1u)) {
+                const unsigned bit = 1u << j;
+                if (!(nonconst & bit)) {
                     const double vv = chunk_val[j];
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv);
-                } else if (!((fallback >> j) & 1u)) {
+                } else if (single & bit) {
+                    // Branch-free per clock: one integer compare + select.
+                    const int thr = chunk_code[j];
+                    const double lv = chunk_val[j], rv = chunk_valr[j];
+                    if (on_mem & bit) {
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], memv[i] <= thr ? lv : rv);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], smv[i] <= thr ? lv : rv);
+                    }
+                } else if (!(fallback & bit)) {
                     const int code = chunk_code[j];
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_dag(pool, code, smv[i], memv[i]));
@@ -426,24 +503,26 @@ template <int CPL, bool kGeneral>
 __global__ void __launch_bounds__(kThreads) grid_select_kernel(const __grid_constant__ GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // Per-warp carve-up: rowE[F], rowT[F], val[32], rn[kRnCap], rl[kRlCap], code[32], counts[2].
+    // Per-warp carve-up: rowE[F], rowT[F], val[32], valr[32], rn[kRnCap],
+    // rl[kRlCap], code[32], counts[2] (see grid_smem_per_warp).
     const int F = p.n_cols;
-    const size_t per_warp = (kGeneral ? 0 : (2 * static_cast<size_t>(F) * 8 + 32 * 8 + kRnCap * 16 + kRlCap * 8 +
-                                             32 * 4 + 16));
+    const size_t per_warp = kGeneral ? 0 : grid_smem_per_warp(F);
     unsigned char* base = smem + per_warp * warp;
     double* rowE = reinterpret_cast<double*>(base);
     double* rowT = rowE + F;
     double* chunk_val = rowT + F;
+    double* chunk_valr = chunk_val + 32;
     WarpPool pool;
-    pool.rn = reinterpret_cast<int4*>(chunk_val + 32);
+    pool.rn = reinterpret_cast<int4*>(chunk_valr + 32);
     pool.rl = reinterpret_cast<double*>(pool.rn + kRnCap);
     int* chunk_code = reinterpret_cast<int*>(pool.rl + kRlCap);
     pool.counts = chunk_code + 32;
 
+    // Lane l owns the contiguous catalog clocks l*CPL .. l*CPL+CPL-1.
     int smv[CPL], memv[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
-        const int c = lane + 32 * i;
+        const int c = lane * CPL + i;
         smv[i] = c < p.n_clocks ? __ldg(p.sm + c) : 0;
         memv[i] = c < p.n_clocks ? __ldg(p.mem + c) : 0;
     }
@@ -463,7 +542,7 @@ __global__ void __launch_bounds__(kThreads) grid_select_kernel(const __grid_cons
             const double* rT[CPL];
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
-                const int c = lane + 32 * i;
+                const int c = lane * CPL + i;
                 const int64_t rec = c < p.n_clocks
                                         ? (p.rec_of_clock ? __ldg(p.rec_of_clock + a * p.n_clocks + c) : a)
                                         : 0;
@@ -493,8 +572,8 @@ __global__ void __launch_bounds__(kThreads) grid_select_kernel(const __grid_cons
             __syncwarp();
             for (int k = lane; k < p.n_cat; k += 32) rowT[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
-            accumulate_model<CPL>(me, rowE, p, pool, chunk_val, chunk_code, smv, memv, lane, accE);
-            accumulate_model<CPL>(mt, rowT, p, pool, chunk_val, chunk_code, smv, memv, lane, accT);
+            accumulate_model<CPL>(me, rowE, p, pool, chunk_val, chunk_valr, chunk_code, smv, memv, lane, accE);
+            accumulate_model<CPL>(mt, rowT, p, pool, chunk_val, chunk_valr, chunk_code, smv, memv, lane, accT);
         }
 
         double E[CPL], T[CPL];
@@ -502,7 +581,7 @@ __global__ void __launch_bounds__(kThreads) grid_select_kernel(const __grid_cons
         for (int i = 0; i < CPL; ++i) {
             E[i] = clamp_energy(finish(p.e_base, p.e_lr, accE[i]));
             T[i] = finish(p.t_base, p.t_lr, accT[i]);
-            const int c = lane + 32 * i;
+            const int c = lane * CPL + i;
             if (c < p.n_clocks) {
                 if (p.e_out) p.e_out[a * p.n_clocks + c] = E[i];
                 if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
@@ -519,7 +598,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const __grid_constant_
     int smv[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
-        const int c = lane + 32 * i;
+        const int c = lane * CPL + i;
         smv[i] = c < p.n_clocks ? __ldg(p.sm + c) : 0;
     }
     for (int64_t a = static_cast<int64_t>(blockIdx.x) * kWarps + warp; a < p.n_apps;
@@ -527,7 +606,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const __grid_constant_
         double E[CPL], T[CPL];
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-            const int c = lane + 32 * i;
+            const int c = lane * CPL + i;
             E[i] = c < p.n_clocks ? __ldg(p.energy + a * p.n_clocks + c) : 0.0;
             T[i] = c < p.n_clocks ? __ldg(p.time + a * p.n_clocks + c) : 0.0;
         }
@@ -566,8 +645,7 @@ int grid_blocks(int64_t units_per_block_work, int64_t n, int sm_count, int block
 
 template <int CPL, bool kGeneral>
 int launch_grid_cpl(const GridParams& p, int sm_count, cudaStream_t stream) {
-    const size_t per_warp = kGeneral ? 0 : (2 * static_cast<size_t>(p.n_cols) * 8 + 32 * 8 + kRnCap * 16 +
-                                            kRlCap * 8 + 32 * 4 + 16);
+    const size_t per_warp = kGeneral ? 0 : grid_smem_per_warp(p.n_cols);
     const size_t smem = per_warp * kWarps;
     auto kern = grid_select_kernel<CPL, kGeneral>;
     if (smem > 48 * 1024) {
