@@ -480,6 +480,9 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
         if (g->sm_clock[c] <= 0 || g->mem_clock[c] <= 0) {
             return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: clock frequencies must be positive");
         }
+        if (g->sm_clock[c] > 65535 || g->mem_clock[c] > 65535) {
+            return set_error(GD_ERR_UNSUPPORTED, "grid_select: clock frequencies above 65535 MHz");
+        }
     }
     for (int32_t k = 0; k < g->n_cat; ++k) {
         if (g->cat_cols[k] < 0 || g->cat_cols[k] >= g->n_cols) {

@@ -1,77 +1,19 @@
-// gd_kernels.cu -- hand-written sm_100a kernels for the (app x clock) path.
+// gd_kernels.cu -- sm_100a kernels other than the fused grid (gd_grid.cu).
 //
 //   K1  predict_gbt / predict_linear   models::predict over materialised rows
 //                                      (models.cpp:395-428, :370-377, :71-78)
-//   K2+K3 grid_select                  ModelPredictorState::build's rows
-//                                      generated on the fly + 2x predict
-//                                      (scheduler.cpp:329-370) fused with the
-//                                      selection of decide()
-//                                      (scheduler.cpp:54-100, 187-234)
 //   K3  select                         selection over given E/T tables
+//                                      (scheduler.cpp:54-100, 212-223)
+//   build_rows_t                       time-encoded rows for the general grid
+//   dadd_probe                         FP64 add-pipe peak for the roofline
 //
-// Bit-exactness rules: node test `x <= thr` in IEEE
-// double; leaves summed in tree order into a double accumulator with
-// __dadd_rn; `base + lr*acc` as __dmul_rn then __dadd_rn (never an FMA);
-// energy clamp `(0.0 < v) ? v : 0.0`; power objective `E / max(T, 1e-12)`
-// with __ddiv_rn.  Tree-level parallelism is used only for traversal; every
-// sum stays sequential per (row, model).
-//
-// No tensor cores: tree traversal is not a contraction.  The grid kernel is
-// bound by the irreducible in-order FP64 adds (2 x n_trees per candidate),
-// see DESIGN.md.
-#include <cuda_runtime.h>
-
-#include <cfloat>
-#include <climits>
-#include <cstdint>
-
-#include "gd_device.cuh"
+// No tensor cores: tree traversal is not a contraction.
+#include "gd_common.cuh"
 
 namespace gd {
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
-constexpr int kWarps = 8;            // warps per CTA for the grid / select kernels
-constexpr int kThreads = kWarps * 32;
-constexpr int kRnCap = 128;          // reduced clock-node slots per warp per 32-tree chunk
-constexpr int kRlCap = 256;          // reduced leaf slots per warp per chunk
-constexpr int kStack = 24;           // DFS stack (>= max depth + 1 for depth <= 23)
-
-// Shared memory of one warp in the partial-evaluation grid kernel:
-// rowE[F] + rowT[F] doubles, val[32] + valr[32] doubles, the residue pool
-// (kRnCap int4 + kRlCap doubles), code[32] ints, 2 counters (16 B padded).
-__host__ __device__ constexpr size_t grid_smem_per_warp(int n_cols) {
-    return 2 * static_cast<size_t>(n_cols) * 8 + 64 * 8 + kRnCap * 16 + kRlCap * 8 + 32 * 4 + 16;
-}
-
-__device__ __forceinline__ void load_node(const PNode* __restrict__ nodes, int32_t n, double& v, int32_t& feat,
-                                          int32_t& aux) {
-    const int4 q = __ldg(reinterpret_cast<const int4*>(nodes) + n);
-    v = __hiloint2double(q.y, q.x);
-    feat = q.z;
-    aux = q.w;
-}
-
-// models.cpp:424  std::max(0.0, v)
-__device__ __forceinline__ double clamp_energy(double v) { return (0.0 < v) ? v : 0.0; }
-
-// models.cpp:419 + 376: base + (lr * acc), two roundings, no contraction.
-__device__ __forceinline__ double finish(double base, double lr, double acc) {
-    return __dadd_rn(base, __dmul_rn(lr, acc));
-}
-
-// scheduler.cpp:54-57
-__device__ __forceinline__ double objective_value(double e, double t, int objective) {
-    if (objective == GD_OBJECTIVE_POWER) return __ddiv_rn(e, (t < 1e-12) ? 1e-12 : t);
-    return e;
-}
-
-// (double)clk <= thr  <=>  clk <= thr_to_int(thr)  for clk > INT_MIN.
-__device__ __forceinline__ int thr_to_int(double thr) {
-    if (!(thr >= -2147483648.0)) return INT_MIN;  // NaN or below int range: never <=
-    if (thr >= 2147483647.0) return INT_MAX;
-    return static_cast<int>(floor(thr));
-}
+using namespace dev;
 
 // ---------------------------------------------------------------------------
 // K1: warp per row, lane per tree (32 trees in flight), then the 32 leaf
@@ -147,462 +89,19 @@ __global__ void build_rows_t_kernel(const double* __restrict__ rows, const doubl
     }
 }
 
-// ---------------------------------------------------------------------------
-// Selection epilogue (K3): lane l owns catalog clocks l, l+32, ...
-// ---------------------------------------------------------------------------
-struct Cand {
-    double obj, t, e;
-    int sm, idx;  // idx < 0: none
-};
-
-// select_text's replacement rule (scheduler.cpp:73-75) closed over catalog
-// order: for finite values the scan returns the argmin of (obj, T, sm, idx).
-__device__ __forceinline__ bool text_less(const Cand& a, const Cand& b) {
-    if (a.idx < 0) return false;
-    if (b.idx < 0) return true;
-    if (a.obj < b.obj) return true;
-    if (a.obj != b.obj) return false;
-    if (a.t < b.t) return true;
-    if (a.t != b.t) return false;
-    if (a.sm < b.sm) return true;
-    if (a.sm != b.sm) return false;
-    return a.idx < b.idx;
-}
-
-// best-effort fastest clock (scheduler.cpp:215-220): argmin (T, E, idx).
-__device__ __forceinline__ bool fast_less(const Cand& a, const Cand& b) {
-    if (a.idx < 0) return false;
-    if (b.idx < 0) return true;
-    if (a.t < b.t) return true;
-    if (a.t != b.t) return false;
-    if (a.e < b.e) return true;
-    if (a.e != b.e) return false;
-    return a.idx < b.idx;
-}
-
-__device__ __forceinline__ Cand shfl_cand(const Cand& c, int mask) {
-    Cand o;
-    o.obj = __shfl_xor_sync(kFull, c.obj, mask);
-    o.t = __shfl_xor_sync(kFull, c.t, mask);
-    o.e = __shfl_xor_sync(kFull, c.e, mask);
-    o.sm = __shfl_xor_sync(kFull, c.sm, mask);
-    o.idx = __shfl_xor_sync(kFull, c.idx, mask);
-    return o;
-}
-
+// K3 alone: warp per app over given candidate tables.
 template <int CPL>
-__device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const double (&T)[CPL], const int (&smv)[CPL],
-                                                int lane, int n_clocks, double budget, int mode, int objective,
-                                                int best_effort, gd_decision* out) {
-    Cand best;
-    best.idx = -1;
-    best.obj = best.t = best.e = 0.0;
-    best.sm = 0;
-    if (mode == GD_MODE_TEXT) {
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            const int c = lane * CPL + i;
-            if (c < n_clocks && !(T[i] > budget)) {
-                Cand k{objective_value(E[i], T[i], objective), T[i], E[i], smv[i], c};
-                if (text_less(k, best)) best = k;
-            }
-        }
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) {
-            Cand o = shfl_cand(best, m);
-            if (text_less(o, best)) best = o;
-        }
-    } else {
-        // scheduler.cpp:86-100: sequential scan in catalog order, DBL_MAX
-        // init, bound tightened to each accepted candidate's time.  Every lane
-        // runs the same scan on broadcast values (lane l owns clocks
-        // l*CPL .. l*CPL+CPL-1, so lane-major order is catalog order).
-        double min_objective = DBL_MAX, max_time = budget;
-        for (int l = 0; l < 32; ++l) {
-            if (l * CPL >= n_clocks) break;
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                const int c = l * CPL + i;
-                const double e = __shfl_sync(kFull, E[i], l);
-                const double t = __shfl_sync(kFull, T[i], l);
-                if (c >= n_clocks) continue;
-                const double value = objective_value(e, t, objective);
-                if (value < min_objective && t <= max_time) {
-                    min_objective = value;
-                    max_time = t;
-                    best.idx = c;
-                    best.e = e;
-                    best.t = t;
-                }
-            }
-        }
-    }
-    int note = GD_NOTE_NONE;
-    if (best.idx < 0 && best_effort) {
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            const int c = lane * CPL + i;
-            if (c < n_clocks) {
-                Cand k{0.0, T[i], E[i], smv[i], c};
-                if (fast_less(k, best)) best = k;
-            }
-        }
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) {
-            Cand o = shfl_cand(best, m);
-            if (fast_less(o, best)) best = o;
-        }
-        note = GD_NOTE_BEST_EFFORT;
-    }
-    if (lane == 0) {
-        gd_decision d;
-        d.clock_index = best.idx;
-        d.status = best.idx >= 0 ? GD_SCHEDULED : GD_REJECTED;
-        d.note = best.idx >= 0 ? note : GD_NOTE_NONE;
-        d.energy_ws = best.idx >= 0 ? best.e : 0.0;
-        d.time_s = best.idx >= 0 ? best.t : 0.0;
-        *out = d;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K2 helpers: per-app partial evaluation of one tree.
-//
-// For one app every candidate row is identical except the two clock
-// columns, so every non-clock node test has the same outcome for all C
-// clocks.  Phase 1 (lane per tree) walks the row-only path until the first
-// clock node; if it ends on a leaf the tree contributes one constant to all
-// C accumulators.  Otherwise the lane expands the tree's clock-only residue:
-// a small DAG of (sm|mem, integer threshold) tests whose ends are leaves,
-// each edge again followed along the row-only path.  Phase 2 (lane per
-// clock) evaluates that residue with integer compares.  The leaf each
-// candidate reaches is exactly predict_row's leaf, so sums stay bit-exact.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int32_t walk_row(const PNode* __restrict__ nodes, int32_t n, const double* row,
-                                            int sm_col, int mem_col, double& v, int32_t& feat, int32_t& aux) {
-    while (true) {
-        load_node(nodes, n, v, feat, aux);
-        if (feat < 0 || feat == sm_col || feat == mem_col) return n;
-        n = (row[feat] <= v) ? aux : aux + 1;
-    }
-}
-
-struct WarpPool {
-    int4* rn;      // {kind 0=sm 1=mem, int thr, lo code, hi code}; code<0: ~leaf slot
-    double* rl;    // reduced leaf values
-    int* counts;   // [0] rn used, [1] rl used
-};
-
-enum : int { kConst = 0, kSingle = 1, kDag = 2, kFallback = 3 };
-
-__device__ __forceinline__ bool stops(int32_t feat, int sm_col, int mem_col) {
-    return feat < 0 || feat == sm_col || feat == mem_col;
-}
-
-// Two independent row-only walks advanced together (ILP for the two
-// continuations below a clock node).
-__device__ __forceinline__ void walk_row2(const PNode* __restrict__ nodes, int32_t a, int32_t b, const double* row,
-                                          int sm_col, int mem_col, double& va, int32_t& fa, double& vb,
-                                          int32_t& fb) {
-    int32_t xa, xb;
-    load_node(nodes, a, va, fa, xa);
-    load_node(nodes, b, vb, fb, xb);
-    bool da = stops(fa, sm_col, mem_col), db = stops(fb, sm_col, mem_col);
-    while (!(da && db)) {
-        if (!da) a = (row[fa] <= va) ? xa : xa + 1;
-        if (!db) b = (row[fb] <= vb) ? xb : xb + 1;
-        if (!da) {
-            load_node(nodes, a, va, fa, xa);
-            da = stops(fa, sm_col, mem_col);
-        }
-        if (!db) {
-            load_node(nodes, b, vb, fb, xb);
-            db = stops(fb, sm_col, mem_col);
-        }
-    }
-}
-
-// General residue: the clock-only DAG below clock node `first`, built into
-// the warp's pool by an explicit DFS.  Returns kDag (code = residue root) or
-// kFallback (code = first; pool or stack exhausted).
-__device__ __noinline__ int reduce_residue(const PNode* __restrict__ nodes, int32_t first, const double* row,
-                                           int sm_col, int mem_col, const WarpPool& pool, int& code) {
-    double v;
-    int32_t feat, aux;
-    load_node(nodes, first, v, feat, aux);
-    const int r0 = atomicAdd(&pool.counts[0], 1);
-    if (r0 >= kRnCap) {
-        code = first;
-        return kFallback;
-    }
-    pool.rn[r0] = make_int4(feat == mem_col ? 1 : 0, thr_to_int(v), 0, 0);
-    int2 stack[kStack];
-    int sp = 0;
-    stack[sp++] = make_int2(r0 * 2 + 1, aux + 1);
-    stack[sp++] = make_int2(r0 * 2 + 0, aux);
-    while (sp > 0) {
-        const int2 task = stack[--sp];
-        walk_row(nodes, task.y, row, sm_col, mem_col, v, feat, aux);
-        int child;
-        if (feat < 0) {
-            const int li = atomicAdd(&pool.counts[1], 1);
-            if (li >= kRlCap) {
-                code = first;
-                return kFallback;
-            }
-            pool.rl[li] = v;
-            child = ~li;
-        } else {
-            const int ri = atomicAdd(&pool.counts[0], 1);
-            if (ri >= kRnCap || sp + 2 > kStack) {
-                code = first;
-                return kFallback;
-            }
-            pool.rn[ri] = make_int4(feat == mem_col ? 1 : 0, thr_to_int(v), 0, 0);
-            stack[sp++] = make_int2(ri * 2 + 1, aux + 1);
-            stack[sp++] = make_int2(ri * 2 + 0, aux);
-            child = ri;
-        }
-        reinterpret_cast<int*>(pool.rn)[(task.x >> 1) * 4 + 2 + (task.x & 1)] = child;
-    }
-    code = r0;
-    return kDag;
-}
-
-// Phase 1 for one tree.  kConst: val = the leaf every candidate reaches.
-// kSingle (the common non-constant case): one clock test separates two
-// leaves -- val/valr = left/right leaf, code = integer threshold, memkind =
-// the test is on mem_clock.  kDag / kFallback: see reduce_residue.
-__device__ __forceinline__ int classify_tree(const PNode* __restrict__ nodes, int32_t root, const double* row,
-                                             int sm_col, int mem_col, const WarpPool& pool, double& val,
-                                             double& valr, int& code, bool& memkind) {
-    double v;
-    int32_t feat, aux;
-    const int32_t first = walk_row(nodes, root, row, sm_col, mem_col, v, feat, aux);
-    if (feat < 0) {
-        val = v;
-        return kConst;
-    }
-    memkind = feat == mem_col;
-    double vl, vr;
-    int32_t fl, fr;
-    walk_row2(nodes, aux, aux + 1, row, sm_col, mem_col, vl, fl, vr, fr);
-    if (fl < 0 && fr < 0) {
-        val = vl;
-        valr = vr;
-        code = thr_to_int(v);
-        return kSingle;
-    }
-    return reduce_residue(nodes, first, row, sm_col, mem_col, pool, code);
-}
-
-__device__ __forceinline__ double eval_dag(const WarpPool& pool, int code, int sm, int mem) {
-    while (code >= 0) {
-        const int4 r = pool.rn[code];
-        const int x = r.x ? mem : sm;
-        code = (x <= r.y) ? r.z : r.w;
-    }
-    return pool.rl[~code];
-}
-
-// Full per-candidate traversal from node n (row + clock override).
-__device__ __forceinline__ double eval_full(const PNode* __restrict__ nodes, int32_t n, const double* row,
-                                            int sm_col, int mem_col, int sm, int mem) {
-    double v;
-    int32_t feat, aux;
-    while (true) {
-        load_node(nodes, n, v, feat, aux);
-        if (feat < 0) return v;
-        const double x = (feat == sm_col) ? static_cast<double>(sm)
-                                          : (feat == mem_col) ? static_cast<double>(mem) : row[feat];
-        n = (x <= v) ? aux : aux + 1;
-    }
-}
-
-struct ModelRef {
-    const PNode* nodes;
-    const int32_t* roots;
-    int32_t n_trees;
-};
-
-// All trees of one model for one app (partial-evaluation path).
-template <int CPL>
-__device__ __forceinline__ void accumulate_model(const ModelRef m, const double* row, const GridParams& p,
-                                                 const WarpPool& pool, double* chunk_val, double* chunk_valr,
-                                                 int* chunk_code, const int (&smv)[CPL], const int (&memv)[CPL],
-                                                 int lane, double (&acc)[CPL]) {
-    for (int32_t t0 = 0; t0 < m.n_trees; t0 += 32) {
-        const int32_t t = t0 + lane;
-        int kind = kConst;
-        bool memkind = false;
-        if (lane == 0) {
-            pool.counts[0] = 0;
-            pool.counts[1] = 0;
-        }
-        __syncwarp();
-        if (t < m.n_trees) {
-            double val = 0.0, valr = 0.0;
-            int code = 0;
-            kind = classify_tree(m.nodes, __ldg(m.roots + t), row, p.sm_col, p.mem_col, pool, val, valr, code,
-                                 memkind);
-            chunk_val[lane] = val;
-            chunk_valr[lane] = valr;
-            chunk_code[lane] = code;
-        }
-        const unsigned nonconst = __ballot_sync(kFull, kind != kConst);
-        const unsigned single = __ballot_sync(kFull, kind == kSingle);
-        const unsigned on_mem = __ballot_sync(kFull, kind == kSingle && memkind);
-        const unsigned fallback = __ballot_sync(kFull, kind == kFallback);
-        __syncwarp();
-        const int nt = min(32, m.n_trees - t0);
-        if (nonconst == 0u && nt == 32) {
-            // Every tree of the chunk is constant over the grid.
-#pragma unroll 4
-            for (int j = 0; j < 32; j += 2) {
-                const double2 vv = *reinterpret_cast<const double2*>(chunk_val + j);
-#pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv.x);
-#pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv.y);
-            }
-        } else {
-            for (int j = 0; j < nt; ++j) {
-                const unsigned bit = 1u << j;
-                if (!(nonconst & bit)) {
-                    const double vv = chunk_val[j];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv);
-                } else if (single & bit) {
-                    // Branch-free per clock: one integer compare + select.
-                    const int thr = chunk_code[j];
-                    const double lv = chunk_val[j], rv = chunk_valr[j];
-                    if (on_mem & bit) {
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], memv[i] <= thr ? lv : rv);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], smv[i] <= thr ? lv : rv);
-                    }
-                } else if (!(fallback & bit)) {
-                    const int code = chunk_code[j];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_dag(pool, code, smv[i], memv[i]));
-                } else {
-                    const int32_t n = chunk_code[j];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i)
-                        acc[i] = __dadd_rn(acc[i], eval_full(m.nodes, n, row, p.sm_col, p.mem_col, smv[i], memv[i]));
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-template <int CPL, bool kGeneral>
-__global__ void __launch_bounds__(kThreads) grid_select_kernel(const __grid_constant__ GridParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ SelectParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // Per-warp carve-up: rowE[F], rowT[F], val[32], valr[32], rn[kRnCap],
-    // rl[kRlCap], code[32], counts[2] (see grid_smem_per_warp).
-    const int F = p.n_cols;
-    const size_t per_warp = kGeneral ? 0 : grid_smem_per_warp(F);
-    unsigned char* base = smem + per_warp * warp;
-    double* rowE = reinterpret_cast<double*>(base);
-    double* rowT = rowE + F;
-    double* chunk_val = rowT + F;
-    double* chunk_valr = chunk_val + 32;
-    WarpPool pool;
-    pool.rn = reinterpret_cast<int4*>(chunk_valr + 32);
-    pool.rl = reinterpret_cast<double*>(pool.rn + kRnCap);
-    int* chunk_code = reinterpret_cast<int*>(pool.rl + kRlCap);
-    pool.counts = chunk_code + 32;
-
-    // Lane l owns the contiguous catalog clocks l*CPL .. l*CPL+CPL-1.
-    int smv[CPL], memv[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-        const int c = lane * CPL + i;
-        smv[i] = c < p.n_clocks ? __ldg(p.sm + c) : 0;
-        memv[i] = c < p.n_clocks ? __ldg(p.mem + c) : 0;
-    }
-    const ModelRef me{p.e_nodes, p.e_roots, p.e_trees};
-    const ModelRef mt{p.t_nodes, p.t_roots, p.t_trees};
-
-    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kWarps + warp; a < p.n_apps;
-         a += static_cast<int64_t>(gridDim.x) * kWarps) {
-        double accE[CPL], accT[CPL];
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) accE[i] = accT[i] = 0.0;
-
-        if constexpr (kGeneral) {
-            // Rows genuinely differ per clock (nearest-record substitution
-            // from several profiled records): full traversal per candidate.
-            const double* rE[CPL];
-            const double* rT[CPL];
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                const int c = lane * CPL + i;
-                const int64_t rec = c < p.n_clocks
-                                        ? (p.rec_of_clock ? __ldg(p.rec_of_clock + a * p.n_clocks + c) : a)
-                                        : 0;
-                rE[i] = p.rows + rec * F;
-                rT[i] = p.rows_t + rec * F;
-            }
-            for (int32_t t = 0; t < me.n_trees; ++t) {
-                const int32_t root = __ldg(me.roots + t);
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    accE[i] = __dadd_rn(accE[i], eval_full(me.nodes, root, rE[i], p.sm_col, p.mem_col, smv[i], memv[i]));
-            }
-            for (int32_t t = 0; t < mt.n_trees; ++t) {
-                const int32_t root = __ldg(mt.roots + t);
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    accT[i] = __dadd_rn(accT[i], eval_full(mt.nodes, root, rT[i], p.sm_col, p.mem_col, smv[i], memv[i]));
-            }
-        } else {
-            __syncwarp();
-            const double* src = p.rows + a * F;
-            for (int j = lane; j < F; j += 32) {
-                const double x = __ldg(src + j);
-                rowE[j] = x;
-                rowT[j] = x;
-            }
-            __syncwarp();
-            for (int k = lane; k < p.n_cat; k += 32) rowT[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
-            __syncwarp();
-            accumulate_model<CPL>(me, rowE, p, pool, chunk_val, chunk_valr, chunk_code, smv, memv, lane, accE);
-            accumulate_model<CPL>(mt, rowT, p, pool, chunk_val, chunk_valr, chunk_code, smv, memv, lane, accT);
-        }
-
-        double E[CPL], T[CPL];
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            E[i] = clamp_energy(finish(p.e_base, p.e_lr, accE[i]));
-            T[i] = finish(p.t_base, p.t_lr, accT[i]);
-            const int c = lane * CPL + i;
-            if (c < p.n_clocks) {
-                if (p.e_out) p.e_out[a * p.n_clocks + c] = E[i];
-                if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
-            }
-        }
-        select_epilogue<CPL>(E, T, smv, lane, p.n_clocks, __ldg(p.budgets + a), p.mode, p.objective,
-                             p.best_effort, p.out + a);
-    }
-}
-
-template <int CPL>
-__global__ void __launch_bounds__(kThreads) select_kernel(const __grid_constant__ SelectParams p) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
     int smv[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
         const int c = lane * CPL + i;
         smv[i] = c < p.n_clocks ? __ldg(p.sm + c) : 0;
     }
-    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kWarps + warp; a < p.n_apps;
-         a += static_cast<int64_t>(gridDim.x) * kWarps) {
+    for (int64_t a = static_cast<int64_t>(blockIdx.x) * wpb + warp; a < p.n_apps;
+         a += static_cast<int64_t>(gridDim.x) * wpb) {
         double E[CPL], T[CPL];
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
@@ -635,48 +134,12 @@ __global__ void __launch_bounds__(256) dadd_probe_kernel(double* out, int iters,
     if (r == 1.2345) out[blockIdx.x] = r;  // keep the chains live
 }
 
-int grid_blocks(int64_t units_per_block_work, int64_t n, int sm_count, int blocks_per_sm) {
-    int64_t want = (n + units_per_block_work - 1) / units_per_block_work;
-    int64_t cap = static_cast<int64_t>(sm_count) * (blocks_per_sm > 0 ? blocks_per_sm : 1);
-    if (want > cap) want = cap;
-    if (want < 1) want = 1;
-    return static_cast<int>(want);
-}
-
-template <int CPL, bool kGeneral>
-int launch_grid_cpl(const GridParams& p, int sm_count, cudaStream_t stream) {
-    const size_t per_warp = kGeneral ? 0 : grid_smem_per_warp(p.n_cols);
-    const size_t smem = per_warp * kWarps;
-    auto kern = grid_select_kernel<CPL, kGeneral>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-    const int blocks = grid_blocks(kWarps, p.n_apps, sm_count, per_sm);
-    kern<<<blocks, kThreads, smem, stream>>>(p);
-    return cudaGetLastError();
-}
-
-template <bool kGeneral>
-int launch_grid_dispatch(const GridParams& p, int sm_count, cudaStream_t s) {
-    const int cpl = (p.n_clocks + 31) / 32;
-    if (cpl <= 1) return launch_grid_cpl<1, kGeneral>(p, sm_count, s);
-    if (cpl <= 2) return launch_grid_cpl<2, kGeneral>(p, sm_count, s);
-    if (cpl <= 4) return launch_grid_cpl<4, kGeneral>(p, sm_count, s);
-    if (cpl <= 7) return launch_grid_cpl<7, kGeneral>(p, sm_count, s);
-    if (cpl <= 9) return launch_grid_cpl<9, kGeneral>(p, sm_count, s);
-    if (cpl <= 12) return launch_grid_cpl<12, kGeneral>(p, sm_count, s);
-    return launch_grid_cpl<16, kGeneral>(p, sm_count, s);
-}
-
 template <int CPL>
 int launch_select_cpl(const SelectParams& p, int sm_count, cudaStream_t stream) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<CPL>, kThreads, 0);
-    const int blocks = grid_blocks(kWarps, p.n_apps, sm_count, per_sm);
-    select_kernel<CPL><<<blocks, kThreads, 0, stream>>>(p);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_kernel<CPL>, 256, 0);
+    const int blocks = grid_blocks(8, p.n_apps, sm_count, per_sm);
+    select_kernel<CPL><<<blocks, 256, 0, stream>>>(p);
     return cudaGetLastError();
 }
 
@@ -718,11 +181,6 @@ int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* 
     build_rows_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, cat_t, cat_cols, n_cat,
                                                                               n_records, n_cols, rows_t);
     return cudaGetLastError();
-}
-
-int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream) {
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    return general ? launch_grid_dispatch<true>(p, sm_count, s) : launch_grid_dispatch<false>(p, sm_count, s);
 }
 
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream) {
