@@ -109,6 +109,8 @@ int upload_model(gd_model* m) {
 }
 
 void release_model(gd_model* m) {
+    if (m->d_grid_nodes) cudaFree(m->d_grid_nodes);
+    m->d_grid_nodes = nullptr;
     if (m->d_nodes) cudaFree(m->d_nodes);
     if (m->d_roots) cudaFree(m->d_roots);
     if (m->d_coef) cudaFree(m->d_coef);
@@ -172,15 +174,39 @@ int validate_grid(const gd_model* me, const gd_model* mt, const gd_grid* g, cons
     return GD_OK;
 }
 
+// The partial-evaluation kernel walks a copy of the packed nodes whose clock
+// columns are recoded (gd_device.cuh kFeatSm / kFeatMem); built once per
+// (model, sm_col, mem_col) on the context stream.
+int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t mem_col) {
+    if (m->d_grid_nodes && m->grid_sm_col == sm_col && m->grid_mem_col == mem_col) return GD_OK;
+    if (m->packed_nodes == 0) return GD_OK;
+    if (!m->d_grid_nodes) {
+        GD_CUDA(cudaMalloc(&m->d_grid_nodes, static_cast<size_t>(m->packed_nodes) * sizeof(gd::PNode)),
+                "cudaMalloc(grid nodes)");
+    }
+    int e = gd::launch_recode_clock_nodes(m->d_nodes, m->d_grid_nodes, m->packed_nodes, sm_col, mem_col, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "recode kernel");
+    m->grid_sm_col = sm_col;
+    m->grid_mem_col = mem_col;
+    return GD_OK;
+}
+
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
               gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t) {
+    const bool general = g.rec_of_clock != nullptr;
+    if (!general) {
+        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col);
+        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col);
+        if (rc) return rc;
+    }
     gd::GridParams p{};
-    p.e_nodes = me->d_nodes;
+    p.e_nodes = general ? me->d_nodes : me->d_grid_nodes;
     p.e_roots = me->d_roots;
     p.e_trees = me->n_trees();
     p.e_base = me->base;
     p.e_lr = me->lr;
-    p.t_nodes = mt->d_nodes;
+    p.t_nodes = general ? mt->d_nodes : mt->d_grid_nodes;
     p.t_roots = mt->d_roots;
     p.t_trees = mt->n_trees();
     p.t_base = mt->base;
@@ -206,7 +232,6 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.objective = o.objective;
     p.best_effort = o.best_effort;
     if (g.n_apps == 0) return GD_OK;
-    const bool general = g.rec_of_clock != nullptr;
     int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");

@@ -22,6 +22,12 @@ struct __align__(16) PNode {
 };
 static_assert(sizeof(PNode) == 16, "PNode must stay 16 bytes");
 
+// In the grid variant of a packed model the clock columns are recoded so one
+// `feat < 0` test stops a row-only walk: leaf -1, sm_clock -2, mem_clock -3.
+constexpr int32_t kFeatLeaf = -1;
+constexpr int32_t kFeatSm = -2;
+constexpr int32_t kFeatMem = -3;
+
 // Everything the fused grid kernel needs, passed as one __grid_constant__.
 struct GridParams {
     const PNode* e_nodes;
@@ -70,6 +76,8 @@ int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* 
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream);
 int launch_select(const SelectParams& p, int sm_count, void* stream);
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
+// Copy `n` packed nodes recoding features sm_col / mem_col as kFeatSm / kFeatMem.
+int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t sm_col, int32_t mem_col, void* stream);
 
 // Largest clock catalog the fused kernels take (32 lanes x 16 clocks).
 constexpr int kMaxClocks = 512;

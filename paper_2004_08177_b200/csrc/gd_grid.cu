@@ -48,13 +48,17 @@ using namespace dev;
 
 constexpr int kWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kThreads = kWarps * 32;
-constexpr int kRnCap = 96;         // residue clock nodes per warp per chunk
-constexpr int kRlCap = 192;        // residue leaves per warp per chunk
+constexpr int kChunk = 64;         // trees per chunk: two independent root walks per lane
+constexpr int kRnCap = 64;         // residue clock nodes per warp per chunk (>= kChunk)
+constexpr int kRlCap = 128;        // residue leaves per warp per chunk
 constexpr int kQCap = 2 * kRnCap;  // queued walks (two per residue node)
 
-// Per warp: row[F] | cval[32] | root[32], first[32] | rn[kRnCap] | rl[kRlCap] | q[kQCap]
+// Per warp: row[F] | cval[64] | root[64], first[64] | rn[kRnCap] | rl[kRlCap] | q[kQCap]
+// (row padded to an even number of doubles so every later array is 16-B aligned)
+__host__ __device__ constexpr int row_slots(int n_cols) { return (n_cols + 1) & ~1; }
 __host__ __device__ constexpr size_t smem_per_warp(int n_cols) {
-    return static_cast<size_t>(n_cols) * 8 + 32 * 8 + 64 * 4 + kRnCap * 16 + kRlCap * 8 + kQCap * 8;
+    return static_cast<size_t>(row_slots(n_cols)) * 8 + kChunk * 8 + 2 * kChunk * 4 + kRnCap * 16 + kRlCap * 8 +
+           kQCap * 8;
 }
 // Per pair: the time warp's T values, 32 lanes x CPL.
 __host__ __device__ constexpr size_t smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
@@ -64,7 +68,7 @@ struct Scratch {
     double* cval;  // constant leaf per tree of the chunk
     int* root;     // residue root (rn index) per tree
     int* first;    // first clock node per tree (fallback start)
-    int4* rn;      // {0 = sm | 1 = mem, packed key, lo code, hi code}; code < 0: ~leaf slot
+    int4* rn;      // {and-mask, packed key, lo code, hi code}; code < 0: ~leaf slot
     double* rl;    // residue leaves
     int2* q;       // {node, dest (rn*2 + side) | tree << 16}
 };
@@ -83,159 +87,256 @@ __device__ __forceinline__ int clock_key(bool on_mem, double thr) {
     return on_mem ? t : static_cast<int>((static_cast<unsigned>(t) << 16) | 0xffffu);
 }
 
-__device__ __forceinline__ bool goes_left(int kind, int key, unsigned ck) {
-    return kind ? ((ck & 0xffffu) <= static_cast<unsigned>(key)) : (ck <= static_cast<unsigned>(key));
+// AND-mask applied to a packed clock before comparing with the key.
+__device__ __forceinline__ int clock_mask(bool on_mem) { return on_mem ? 0xffff : -1; }
+
+__device__ __forceinline__ bool goes_left(int mask, int key, unsigned ck) {
+    return (ck & static_cast<unsigned>(mask)) <= static_cast<unsigned>(key);
 }
 
-__device__ __forceinline__ void walk_row(const PNode* __restrict__ nodes, int32_t n, const double* row, int sm_col,
-                                         int mem_col, double& v, int32_t& feat, int32_t& aux) {
-    while (true) {
-        load_node(nodes, n, v, feat, aux);
-        if (feat < 0 || feat == sm_col || feat == mem_col) return;
-        n = (row[feat] <= v) ? aux : aux + 1;
+__device__ __forceinline__ int4 residue_node(bool on_mem, double thr) {
+    return make_int4(clock_mask(on_mem), clock_key(on_mem, thr), 0, 0);
+}
+
+
+// One row-only walk state: current node, its value / feature / left child.
+struct Walk {
+    int32_t n, feat, aux;
+    double v;
+};
+
+// Two independent row-only walks advanced side by side (two load chains in
+// flight) until each reaches a leaf or a clock node.  Invalid walks are
+// skipped.
+// Nodes are the grid variant (clock columns recoded negative), so a walk
+// stops at the first node with feat < 0.  Loads are unconditional (a
+// finished or invalid walk re-reads its current node) to keep the loop free
+// of predicated moves.
+__device__ __forceinline__ void walk2(const PNode* __restrict__ nodes, bool va, Walk& a, bool vb, Walk& b,
+                                      const double* row) {
+    load_node(nodes, a.n, a.v, a.feat, a.aux);
+    load_node(nodes, b.n, b.v, b.feat, b.aux);
+    bool ga = va && a.feat >= 0, gb = vb && b.feat >= 0;
+    while (ga || gb) {
+        const double xa = row[ga ? a.feat : 0], xb = row[gb ? b.feat : 0];
+        a.n = ga ? ((xa <= a.v) ? a.aux : a.aux + 1) : a.n;
+        b.n = gb ? ((xb <= b.v) ? b.aux : b.aux + 1) : b.n;
+        load_node(nodes, a.n, a.v, a.feat, a.aux);
+        load_node(nodes, b.n, b.v, b.feat, b.aux);
+        ga = ga && a.feat >= 0;
+        gb = gb && b.feat >= 0;
     }
 }
 
-// Phase 1 for the chunk [t0, t0 + nt): fills cval / root / first / rn / rl.
-// Returns the masks of non-constant trees and of trees whose residue did not
-// fit the pool (those fall back to per-clock traversal from `first`).
-__device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int nt, const double* row, int sm_col,
-                                             int mem_col, const Scratch& s, int lane, unsigned& nonconst,
-                                             unsigned& fallback) {
-    const unsigned lt = (1u << lane) - 1u;
-    double v = 0.0;
-    int32_t feat = -1, aux = 0, first = 0;
-    bool clk = false;
-    if (lane < nt) {
-        first = __ldg(m.roots + t0 + lane);
-        while (true) {
-            load_node(m.nodes, first, v, feat, aux);
-            if (feat < 0 || feat == sm_col || feat == mem_col) break;
-            first = (row[feat] <= v) ? aux : aux + 1;
+// Residue pool allocation state of one warp (warp-uniform).
+struct Alloc {
+    int n_rn, n_rl, tail;
+    unsigned fb_lo, fb_hi;
+};
+
+// Record the end of one queued walk per lane (a group of <= 32 items): a leaf
+// becomes a residue leaf, a clock node a residue node with two new queued
+// walks; the parent's child code is patched.  Ballot-prefix allocation keeps
+// each group's allocations in lane order, so what fits is a prefix.  Items
+// that do not fit mark their tree for fallback.
+__device__ __forceinline__ void place(bool have, int2 item, const Walk& w, int mem_col, const Scratch& s, unsigned lt,
+                                      Alloc& al) {
+    const bool leaf = have && w.feat == kFeatLeaf, node = have && w.feat != kFeatLeaf;
+    const unsigned mleaf = __ballot_sync(kFull, leaf);
+    const unsigned mnode = __ballot_sync(kFull, node);
+    const int tree = item.y >> 16, dest = item.y & 0xffff;
+    const int node_room = min(kRnCap - al.n_rn, (kQCap - al.tail) / 2);  // tail, kQCap even
+    bool over = false;
+    int child = 0;
+    if (leaf) {
+        const int li = al.n_rl + __popc(mleaf & lt);
+        if (li < kRlCap) {
+            s.rl[li] = w.v;
+            child = ~li;
+        } else {
+            over = true;
         }
-        if (feat < 0) s.cval[lane] = v;
-        clk = feat >= 0;
     }
-    const unsigned mclk = __ballot_sync(kFull, clk);
-    nonconst = mclk;
+    if (node) {
+        const int p = __popc(mnode & lt);
+        const int ri = al.n_rn + p, q2 = al.tail + 2 * p;
+        if (p < node_room) {
+            s.rn[ri] = residue_node(w.feat == kFeatMem, w.v);
+            s.q[q2] = make_int2(w.aux, (ri * 2) | (tree << 16));
+            s.q[q2 + 1] = make_int2(w.aux + 1, (ri * 2 + 1) | (tree << 16));
+            child = ri;
+        } else {
+            over = true;
+        }
+    }
+    if (have && !over) reinterpret_cast<int*>(s.rn)[(dest >> 1) * 4 + 2 + (dest & 1)] = child;
+    al.fb_lo |= __reduce_or_sync(kFull, over && tree < 32 ? (1u << tree) : 0u);
+    al.fb_hi |= __reduce_or_sync(kFull, over && tree >= 32 ? (1u << (tree - 32)) : 0u);
+    al.n_rl += max(0, min(__popc(mleaf), kRlCap - al.n_rl));
+    const int nodes_fit = max(0, min(__popc(mnode), node_room));
+    al.n_rn += nodes_fit;
+    al.tail += 2 * nodes_fit;
+}
+
+// Phase 1 for the chunk [t0, t0 + nt), nt <= 64: fills cval / root / first /
+// rn / rl.  Lane l walks trees l and 32 + l side by side (two independent
+// load chains).  Returns the masks of non-constant trees and of trees whose
+// residue did not fit the pool (those fall back to per-clock traversal from
+// `first`).
+__device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int nt, const double* row, int sm_col,
+                                             int mem_col, const Scratch& s, int lane, uint64_t& nonconst,
+                                             uint64_t& fallback) {
+    const unsigned lt = (1u << lane) - 1u;
+    const bool va = lane < nt, vb = lane + 32 < nt;
+    Walk a{0, -1, 0, 0.0}, b{0, -1, 0, 0.0};
+    if (va) a.n = __ldg(m.roots + t0 + lane);
+    if (vb) b.n = __ldg(m.roots + t0 + 32 + lane);
+    walk2(m.nodes, va, a, vb, b, row);
+    const bool ca = va && a.feat != kFeatLeaf, cb = vb && b.feat != kFeatLeaf;
+    if (va && !ca) s.cval[lane] = a.v;
+    if (vb && !cb) s.cval[32 + lane] = b.v;
+    const unsigned ma = __ballot_sync(kFull, ca), mb = __ballot_sync(kFull, cb);
+    nonconst = static_cast<uint64_t>(ma) | (static_cast<uint64_t>(mb) << 32);
     fallback = 0u;
-    if (mclk == 0u) return;
-    unsigned fb = 0u;
-    int n_rn = __popc(mclk);  // <= 32 <= kRnCap
-    int tail = 2 * n_rn;      // <= 64 <= kQCap
-    int n_rl = 0;
-    if (clk) {
-        const int idx = __popc(mclk & lt);
-        const bool on_mem = feat == mem_col;
-        s.rn[idx] = make_int4(on_mem ? 1 : 0, clock_key(on_mem, v), 0, 0);
+    if (nonconst == 0u) return;
+    Alloc al;
+    al.n_rn = __popc(ma) + __popc(mb);  // <= 64 <= kRnCap
+    al.tail = 2 * al.n_rn;              // <= 128 <= kQCap
+    al.n_rl = 0;
+    al.fb_lo = al.fb_hi = 0u;
+    if (ca) {
+        const int idx = __popc(ma & lt);
+        s.rn[idx] = residue_node(a.feat == kFeatMem, a.v);
         s.root[lane] = idx;
-        s.first[lane] = first;
-        s.q[2 * idx] = make_int2(aux, (idx * 2) | (lane << 16));
-        s.q[2 * idx + 1] = make_int2(aux + 1, (idx * 2 + 1) | (lane << 16));
+        s.first[lane] = a.n;
+        s.q[2 * idx] = make_int2(a.aux, (idx * 2) | (lane << 16));
+        s.q[2 * idx + 1] = make_int2(a.aux + 1, (idx * 2 + 1) | (lane << 16));
+    }
+    if (cb) {
+        const int idx = __popc(ma) + __popc(mb & lt);
+        s.rn[idx] = residue_node(b.feat == kFeatMem, b.v);
+        s.root[32 + lane] = idx;
+        s.first[32 + lane] = b.n;
+        s.q[2 * idx] = make_int2(b.aux, (idx * 2) | ((32 + lane) << 16));
+        s.q[2 * idx + 1] = make_int2(b.aux + 1, (idx * 2 + 1) | ((32 + lane) << 16));
     }
     __syncwarp();
+    // Breadth-first rounds over the queue, two items per lane per iteration.
     int head = 0;
-    while (head < tail) {
-        const int qi = head + lane;
-        const bool have = qi < tail;
-        int2 item = make_int2(0, 0);
-        bool leaf = false, node = false;
-        if (have) {
-            item = s.q[qi];
-            walk_row(m.nodes, item.x, row, sm_col, mem_col, v, feat, aux);
-            leaf = feat < 0;
-            node = !leaf;
+    while (head < al.tail) {
+        const int end = min(head + 64, al.tail);  // items queued before this iteration
+        const int qa = head + lane, qb = head + 32 + lane;
+        const bool ha = qa < end, hb = qb < end;
+        int2 ia = make_int2(0, 0), ib = make_int2(0, 0);
+        if (ha) {
+            ia = s.q[qa];
+            a.n = ia.x;
         }
-        const unsigned mleaf = __ballot_sync(kFull, leaf);
-        const unsigned mnode = __ballot_sync(kFull, node);
-        const int tree = item.y >> 16, dest = item.y & 0xffff;
-        const int node_room = min(kRnCap - n_rn, (kQCap - tail) / 2);  // tail, kQCap even
-        bool over = false;
-        int child = 0;
-        if (leaf) {
-            const int li = n_rl + __popc(mleaf & lt);
-            if (li < kRlCap) {
-                s.rl[li] = v;
-                child = ~li;
-            } else {
-                over = true;
-            }
+        if (hb) {
+            ib = s.q[qb];
+            b.n = ib.x;
         }
-        if (node) {
-            const int p = __popc(mnode & lt);
-            const int ri = n_rn + p, q2 = tail + 2 * p;
-            if (p < node_room) {
-                const bool on_mem = feat == mem_col;
-                s.rn[ri] = make_int4(on_mem ? 1 : 0, clock_key(on_mem, v), 0, 0);
-                s.q[q2] = make_int2(aux, (ri * 2) | (tree << 16));
-                s.q[q2 + 1] = make_int2(aux + 1, (ri * 2 + 1) | (tree << 16));
-                child = ri;
-            } else {
-                over = true;
-            }
-        }
-        if (have && !over) reinterpret_cast<int*>(s.rn)[(dest >> 1) * 4 + 2 + (dest & 1)] = child;
-        fb |= __reduce_or_sync(kFull, over ? (1u << tree) : 0u);
-        // Allocations that fitted are a prefix of each lane-ordered group.
-        n_rl += max(0, min(__popc(mleaf), kRlCap - n_rl));
-        const int nodes_fit = max(0, min(__popc(mnode), node_room));
-        n_rn += nodes_fit;
-        head = min(head + 32, tail);
-        tail += 2 * nodes_fit;
+        walk2(m.nodes, ha, a, hb, b, row);
+        place(ha, ia, a, mem_col, s, lt, al);
+        place(hb, ib, b, mem_col, s, lt, al);
+        head = end;
         __syncwarp();
     }
-    fallback = fb;
+    fallback = static_cast<uint64_t>(al.fb_lo) | (static_cast<uint64_t>(al.fb_hi) << 32);
 }
 
-// Full per-candidate traversal from node n with a packed clock.
+// Full per-candidate traversal from node n (grid-variant nodes) with a packed
+// clock: predict_row on the substituted row (models.cpp:71-78).
 __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nodes, int32_t n, const double* row,
-                                                   int sm_col, int mem_col, unsigned ck) {
-    return eval_full(nodes, n, row, sm_col, mem_col, static_cast<int>(ck >> 16), static_cast<int>(ck & 0xffffu));
+                                                   unsigned ck) {
+    const double sm = static_cast<double>(ck >> 16), mem = static_cast<double>(ck & 0xffffu);
+    double v;
+    int32_t feat, aux;
+    while (true) {
+        load_node(nodes, n, v, feat, aux);
+        if (feat == kFeatLeaf) return v;
+        const double x = feat >= 0 ? row[feat] : (feat == kFeatSm ? sm : mem);
+        n = (x <= v) ? aux : aux + 1;
+    }
 }
 
 template <int CPL>
 __device__ __forceinline__ void accumulate_model(const ModelRef& m, const double* row, int sm_col, int mem_col,
                                                  const Scratch& s, const unsigned (&ck)[CPL], int lane,
                                                  double (&acc)[CPL]) {
-    for (int32_t t0 = 0; t0 < m.n_trees; t0 += 32) {
-        const int nt = min(32, m.n_trees - t0);
-        unsigned nonconst, fallback;
+    for (int32_t t0 = 0; t0 < m.n_trees; t0 += kChunk) {
+        const int nt = min(kChunk, m.n_trees - t0);
+        uint64_t nonconst, fallback;
         expand_chunk(m, t0, nt, row, sm_col, mem_col, s, lane, nonconst, fallback);
         __syncwarp();
-        int j = 0;
-        while (j < nt) {
-            // Two constant trees at once (one LDS.128), in tree order.
-            if (!(j & 1) && j + 1 < nt && !((nonconst >> j) & 3u)) {
-                const double2 vv = *reinterpret_cast<const double2*>(s.cval + j);
+        for (int h = 0; h < kChunk; h += 32) {
+            const int nth = min(32, nt - h);
+            if (nth <= 0) break;
+            const unsigned nc = static_cast<unsigned>(nonconst >> h);
+            const unsigned fbm = static_cast<unsigned>(fallback >> h);
+            int jj = 0;
+            while (jj < nth) {
+                // A run of constant trees jj .. jj+run-1, then one non-constant tree.
+                const unsigned rest = nc >> jj;
+                const int run = rest ? min(__ffs(rest) - 1, nth - jj) : nth - jj;
+                const double* cv = s.cval + h + jj;
+                int k = 0;
+                for (; k + 1 < run; k += 2) {
+                    const double v0 = cv[k], v1 = cv[k + 1];
 #pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv.x);
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
 #pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv.y);
-                j += 2;
-                continue;
-            }
-            const unsigned bit = 1u << j;
-            if (!(nonconst & bit)) {
-                const double vv = s.cval[j];
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v1);
+                }
+                if (k < run) {
+                    const double v0 = cv[k];
 #pragma unroll
-                for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], vv);
-            } else if (fallback & bit) {
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
+                }
+                jj += run;
+                if (jj >= nth) break;
+                const int j = h + jj;
+                const bool fb_tree = (fbm >> jj) & 1u;
+                ++jj;
+            if (fb_tree) {
                 const int32_t n = s.first[j];
 #pragma unroll
                 for (int i = 0; i < CPL; ++i)
-                    acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, n, row, sm_col, mem_col, ck[i]));
+                    acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, n, row, ck[i]));
             } else {
                 const int4 r = s.rn[s.root[j]];
+                const unsigned key = static_cast<unsigned>(r.y);
                 if (r.z < 0 && r.w < 0) {
                     // One clock test between two leaves: compare + select.
                     const double lv = s.rl[~r.z], rv = s.rl[~r.w];
-                    const unsigned key = static_cast<unsigned>(r.y);
-                    if (r.x) {
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= key ? lv : rv);
-                    } else {
+                    if (r.x == -1) {
 #pragma unroll
                         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= key ? lv : rv);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= key ? lv : rv);
+                    }
+                } else if ((r.z < 0) != (r.w < 0) && s.rn[r.z < 0 ? r.w : r.z].z < 0 &&
+                           s.rn[r.z < 0 ? r.w : r.z].w < 0) {
+                    // Two tests: the root and one child test, three leaves.
+                    const bool node_left = r.z >= 0;
+                    const int4 c = s.rn[node_left ? r.z : r.w];
+                    const double solo = s.rl[~(node_left ? r.w : r.z)];
+                    const double cl = s.rl[~c.z], cr = s.rl[~c.w];
+                    const unsigned rmask = static_cast<unsigned>(r.x), cmask = static_cast<unsigned>(c.x);
+                    const unsigned ckey = static_cast<unsigned>(c.y);
+                    if (node_left) {
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) {
+                            const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
+                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= key ? sub : solo);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) {
+                            const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
+                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= key ? solo : sub);
+                        }
                     }
                 } else {
 #pragma unroll
@@ -249,7 +350,7 @@ __device__ __forceinline__ void accumulate_model(const ModelRef& m, const double
                     }
                 }
             }
-            ++j;
+            }
         }
         __syncwarp();
     }
@@ -258,13 +359,27 @@ __device__ __forceinline__ void accumulate_model(const ModelRef& m, const double
 // Named barrier for one warp pair.  The warp reconverges first (independent
 // thread scheduling does not guarantee it after the data-dependent loops),
 // and the non-.aligned form is used.
-__device__ __forceinline__ void named_sync(int id, int threads) {
+// Barrier ids are immediates: a register id makes ptxas reserve all 16
+// named barriers per CTA, which caps residency at 4 CTAs per SM.
+template <int kId>
+__device__ __forceinline__ void pair_sync() {
     __syncwarp();
-    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+    asm volatile("barrier.sync %0, 64;" ::"n"(kId) : "memory");
+}
+
+// Barrier A (pair 0: id 1, pair 1: id 3) and barrier B (ids 2 / 4).
+__device__ __forceinline__ void pair_sync_a(int pair) {
+    if (pair == 0) pair_sync<1>();
+    else pair_sync<3>();
+}
+__device__ __forceinline__ void pair_sync_b(int pair) {
+    if (pair == 0) pair_sync<2>();
+    else pair_sync<4>();
 }
 
 template <int CPL>
-__global__ void __launch_bounds__(kThreads, GD_GRID_MIN_BLOCKS) grid_partial_kernel(const __grid_constant__ GridParams p) {
+__global__ void __launch_bounds__(kThreads, (CPL >= 12 ? 4 : GD_GRID_MIN_BLOCKS))
+    grid_partial_kernel(const __grid_constant__ GridParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
@@ -273,10 +388,10 @@ __global__ void __launch_bounds__(kThreads, GD_GRID_MIN_BLOCKS) grid_partial_ker
     unsigned char* base = smem + smem_per_warp(F) * warp;
     Scratch s;
     s.row = reinterpret_cast<double*>(base);
-    s.cval = s.row + F;
-    s.root = reinterpret_cast<int*>(s.cval + 32);
-    s.first = s.root + 32;
-    s.rn = reinterpret_cast<int4*>(s.first + 32);
+    s.cval = s.row + row_slots(F);
+    s.root = reinterpret_cast<int*>(s.cval + kChunk);
+    s.first = s.root + kChunk;
+    s.rn = reinterpret_cast<int4*>(s.first + kChunk);
     s.rl = reinterpret_cast<double*>(s.rn + kRnCap);
     s.q = reinterpret_cast<int2*>(s.rl + kRlCap);
     double* tbuf = reinterpret_cast<double*>(smem + smem_per_warp(F) * kWarps + smem_per_pair(CPL) * pair);
@@ -295,7 +410,6 @@ __global__ void __launch_bounds__(kThreads, GD_GRID_MIN_BLOCKS) grid_partial_ker
     m.roots = is_time ? p.t_roots : p.e_roots;
     m.n_trees = is_time ? p.t_trees : p.e_trees;
     const int sm_col = p.sm_col, mem_col = p.mem_col;
-    const int bar_a = 1 + 2 * pair, bar_b = 2 + 2 * pair;
 
     for (int64_t a = static_cast<int64_t>(blockIdx.x) * (kWarps / 2) + pair; a < p.n_apps;
          a += static_cast<int64_t>(gridDim.x) * (kWarps / 2)) {
@@ -313,10 +427,10 @@ __global__ void __launch_bounds__(kThreads, GD_GRID_MIN_BLOCKS) grid_partial_ker
         }
         accumulate_model<CPL>(m, s.row, sm_col, mem_col, s, ck, lane, acc);
         if (is_time) {
-            named_sync(bar_a, 64);  // the energy warp is done reading the previous app's times
+            pair_sync_a(pair);  // the energy warp is done reading the previous app's times
 #pragma unroll
             for (int i = 0; i < CPL; ++i) tbuf[lane * CPL + i] = finish(p.t_base, p.t_lr, acc[i]);
-            named_sync(bar_b, 64);
+            pair_sync_b(pair);
         } else {
             double E[CPL], T[CPL];
             int smv[CPL];
@@ -325,8 +439,8 @@ __global__ void __launch_bounds__(kThreads, GD_GRID_MIN_BLOCKS) grid_partial_ker
                 E[i] = clamp_energy(finish(p.e_base, p.e_lr, acc[i]));
                 smv[i] = static_cast<int>(ck[i] >> 16);
             }
-            named_sync(bar_a, 64);
-            named_sync(bar_b, 64);
+            pair_sync_a(pair);
+            pair_sync_b(pair);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
                 T[i] = tbuf[lane * CPL + i];
@@ -412,6 +526,9 @@ int launch_cpl(const GridParams& p, bool general, int sm_count, cudaStream_t str
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
+    // Occupancy is set by registers (launch bounds); give shared memory the
+    // whole carveout so it never limits resident CTAs.
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     const int blocks = grid_blocks(kWarps / 2, p.n_apps, sm_count, per_sm);

@@ -37,6 +37,10 @@ struct gd_model {
     int32_t* d_roots = nullptr;
     double* d_coef = nullptr;
     int64_t packed_nodes = 0;
+    // Grid variant of d_nodes: the sm / mem clock columns recoded as
+    // feat = kFeatSm / kFeatMem (built on first use per column pair).
+    mutable gd::PNode* d_grid_nodes = nullptr;
+    mutable int32_t grid_sm_col = -1, grid_mem_col = -1;
 
     int32_t n_trees() const { return offsets.empty() ? 0 : static_cast<int32_t>(offsets.size() - 1); }
 };

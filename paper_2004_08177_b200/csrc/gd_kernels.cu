@@ -134,6 +134,19 @@ __global__ void __launch_bounds__(256) dadd_probe_kernel(double* out, int iters,
     if (r == 1.2345) out[blockIdx.x] = r;  // keep the chains live
 }
 
+__global__ void recode_clock_nodes_kernel(const PNode* __restrict__ src, PNode* __restrict__ dst, int64_t n,
+                                          int32_t sm_col, int32_t mem_col) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        PNode x = src[i];
+        if (x.feat >= 0) {
+            if (x.feat == sm_col) x.feat = kFeatSm;
+            else if (x.feat == mem_col) x.feat = kFeatMem;
+        }
+        dst[i] = x;
+    }
+}
+
 template <int CPL>
 int launch_select_cpl(const SelectParams& p, int sm_count, cudaStream_t stream) {
     int per_sm = 0;
@@ -180,6 +193,14 @@ int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* 
     if (blocks < 1) blocks = 1;
     build_rows_t_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, cat_t, cat_cols, n_cat,
                                                                               n_records, n_cols, rows_t);
+    return cudaGetLastError();
+}
+
+int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t sm_col, int32_t mem_col, void* stream) {
+    int blocks = static_cast<int>((n + 255) / 256);
+    if (blocks > 8192) blocks = 8192;
+    if (blocks < 1) blocks = 1;
+    recode_clock_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n, sm_col, mem_col);
     return cudaGetLastError();
 }
 
