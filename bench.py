@@ -44,6 +44,7 @@ def parse_args():
     p.add_argument("--cpu-sample-s", type=float, default=10.0, help="target seconds of CPU baseline work")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling (use under ncu)")
+    p.add_argument("--w-clk", type=float, default=None, help="experiment: clock-split weight of the synthetic trees")
     return p.parse_args()
 
 
@@ -55,10 +56,11 @@ def workload_config(name: str, world: int):
     return cfg, per_rank, per_rank * world
 
 
-def make_inputs(cfg, n_total, seed=1234):
+def make_inputs(cfg, n_total, seed=1234, w_clk=None):
     from paper_2004_08177_b200 import workload as W
 
-    return W.make_scenario("bench", n_total, cfg["catalog"], cfg["n_trees"], cfg["depth"], seed=seed)
+    kw = {} if w_clk is None else {"w_clk": w_clk}
+    return W.make_scenario("bench", n_total, cfg["catalog"], cfg["n_trees"], cfg["depth"], seed=seed, **kw)
 
 
 def config_json(name, cfg, per_rank, world, n_clocks):
@@ -136,7 +138,7 @@ def run_ours(args, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
 
     cfg, per_rank, n_total = workload_config(args.config, world)
-    sc = make_inputs(cfg, n_total)
+    sc = make_inputs(cfg, n_total, w_clk=args.w_clk)
     lo, hi = shard.shard_range(n_total, rank, world)
     A = hi - lo
     g = sc.grid

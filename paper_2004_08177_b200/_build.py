@@ -47,13 +47,15 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = True) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = True, out: Path = None, defines=()) -> Path:
+    """Build lib/libgdvfs.so (or `out` with extra -D `defines`, for experiments)."""
+    lib = Path(out) if out else LIB
+    if not force and out is None and not _stale():
         return LIB
-    objdir = PKG / "lib" / "obj"
+    objdir = lib.parent / ("obj" if out is None else f"obj_{lib.stem}")
     objdir.mkdir(parents=True, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O3,-Wall",
-              f"-I{ROOT / 'include'}", f"-I{CSRC}"] + ccbin() + ARCH
+              f"-I{ROOT / 'include'}", f"-I{CSRC}"] + [f"-D{d}" for d in defines] + ccbin() + ARCH
     cmds, objs = [], []
     for s in SOURCES:
         src = CSRC / s
@@ -68,15 +70,19 @@ def build(force: bool = False, verbose: bool = True) -> Path:
             if verbose:
                 print(" ".join(cmd), flush=True)
         list(pool.map(lambda c: subprocess.run(c, check=True), cmds))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ccbin(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lcudart_static", "-lrt", "-lpthread",
            "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    # python -m paper_2004_08177_b200._build [--force] [--out PATH -DNAME=V ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    build(force="--force" in args, out=out, defines=defs)

@@ -7,9 +7,11 @@ missing or the device is not a Blackwell GPU, calls raise ``GdError``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libgdvfs.so"
+# GDVFS_LIB selects another build of the same library (A/B experiments).
+LIB_PATH = Path(os.environ.get("GDVFS_LIB", Path(__file__).resolve().parent / "lib" / "libgdvfs.so"))
 
 GD_OK = 0
 GD_ERR_INVALID_ARGUMENT = 1

@@ -33,6 +33,8 @@
 // (1 <= sm, mem <= 65535, validated on the host).  A test `(double)sm <= thr`
 // is `ck <= ((clamp(floor(thr), 0, 65535) << 16) | 0xffff)` (unsigned); a test
 // `(double)mem <= thr` is `(ck & 0xffff) <= clamp(floor(thr), 0, 65535)`.
+#include <cstdlib>
+
 #include "gd_common.cuh"
 
 namespace gd {
@@ -41,9 +43,9 @@ namespace {
 using namespace dev;
 
 // Resident CTAs per SM the partial kernel is compiled for (register cap
-// 65536 / (128 * N)); 6 -> 80 registers, 24 warps per SM.
+// 65536 / (128 * N)); 8 -> 64 registers, 32 warps per SM.
 #ifndef GD_GRID_MIN_BLOCKS
-#define GD_GRID_MIN_BLOCKS 6
+#define GD_GRID_MIN_BLOCKS 8
 #endif
 
 constexpr int kWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
@@ -53,24 +55,59 @@ constexpr int kRnCap = 64;         // residue clock nodes per warp per chunk (>=
 constexpr int kRlCap = 128;        // residue leaves per warp per chunk
 constexpr int kQCap = 2 * kRnCap;  // queued walks (two per residue node)
 
-// Per warp: row[F] | cval[64] | root[64], first[64] | rn[kRnCap] | rl[kRlCap] | q[kQCap]
-// (row padded to an even number of doubles so every later array is 16-B aligned)
+// Per warp: row[F] | cval, cv2, cv3 [64] | root, first [64] | ttype[64] |
+// rn[kRnCap] | rl[kRlCap] | q[kQCap] (the per-tree key records alias q once
+// the expansion is done).  The row is padded to an even number of doubles so
+// every later array is 16-B aligned.
 __host__ __device__ constexpr int row_slots(int n_cols) { return (n_cols + 1) & ~1; }
+// Fixed byte offsets inside a warp's region (the row, whose size depends on
+// the column count, goes last) so every array is base + constant: one live
+// register instead of one pointer per array.
+constexpr int kOffCval = 0;
+constexpr int kOffCv2 = kOffCval + kChunk * 8;
+constexpr int kOffCv3 = kOffCv2 + kChunk * 8;
+constexpr int kOffRn = kOffCv3 + kChunk * 8;
+constexpr int kOffRl = kOffRn + kRnCap * 16;
+constexpr int kOffQ = kOffRl + kRlCap * 8;
+constexpr int kOffRoot = kOffQ + kQCap * 8;
+constexpr int kOffFirst = kOffRoot + kChunk * 4;
+constexpr int kOffType = kOffFirst + kChunk * 4;
+constexpr int kOffRow = (kOffType + kChunk + 15) & ~15;
 __host__ __device__ constexpr size_t smem_per_warp(int n_cols) {
-    return static_cast<size_t>(row_slots(n_cols)) * 8 + kChunk * 8 + 2 * kChunk * 4 + kRnCap * 16 + kRlCap * 8 +
-           kQCap * 8;
+    return static_cast<size_t>(kOffRow) + static_cast<size_t>(row_slots(n_cols)) * 8;
 }
+static_assert(kQCap * 8 >= kChunk * 16, "key records alias the queue");
 // Per pair: the time warp's T values, 32 lanes x CPL.
 __host__ __device__ constexpr size_t smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
 
+// Per-tree residue classes resolved after the expansion (phase 2 dispatch).
+enum : unsigned char {
+    kConstTree = 0,
+    kSingleSm = 1,    // cval / cv2 = left / right leaf, key.y = key
+    kSingleMem = 2,
+    kDoubleLeft = 3,  // root test, node child on the left: cval = right leaf,
+    kDoubleRight = 4, //   cv2 / cv3 = child's left / right leaf, key = {rmask, rkey, cmask, ckey}
+    kDagTree = 5,     // key.x = residue root
+    kFallbackTree = 6 // key.x = first clock node
+};
+
 struct Scratch {
-    double* row;
-    double* cval;  // constant leaf per tree of the chunk
-    int* root;     // residue root (rn index) per tree
-    int* first;    // first clock node per tree (fallback start)
-    int4* rn;      // {and-mask, packed key, lo code, hi code}; code < 0: ~leaf slot
-    double* rl;    // residue leaves
-    int2* q;       // {node, dest (rn*2 + side) | tree << 16}
+    unsigned char* base;  // this warp's region
+    // constant leaf per tree of the chunk / record value 0
+    __device__ __forceinline__ double* cval() const { return reinterpret_cast<double*>(base + kOffCval); }
+    __device__ __forceinline__ double* cv2() const { return reinterpret_cast<double*>(base + kOffCv2); }
+    __device__ __forceinline__ double* cv3() const { return reinterpret_cast<double*>(base + kOffCv3); }
+    // residue nodes {and-mask, packed key, lo code, hi code}; code < 0: ~leaf slot
+    __device__ __forceinline__ int4* rn() const { return reinterpret_cast<int4*>(base + kOffRn); }
+    __device__ __forceinline__ double* rl() const { return reinterpret_cast<double*>(base + kOffRl); }
+    // queued walks {node, dest (rn*2 + side) | tree << 16}
+    __device__ __forceinline__ int2* q() const { return reinterpret_cast<int2*>(base + kOffQ); }
+    // per-tree key records (alias the queue once the expansion is done)
+    __device__ __forceinline__ int4* key() const { return reinterpret_cast<int4*>(base + kOffQ); }
+    __device__ __forceinline__ int* root() const { return reinterpret_cast<int*>(base + kOffRoot); }
+    __device__ __forceinline__ int* first() const { return reinterpret_cast<int*>(base + kOffFirst); }
+    __device__ __forceinline__ unsigned char* ttype() const { return base + kOffType; }
+    __device__ __forceinline__ double* row() const { return reinterpret_cast<double*>(base + kOffRow); }
 };
 
 struct ModelRef {
@@ -151,7 +188,7 @@ __device__ __forceinline__ void place(bool have, int2 item, const Walk& w, int m
     if (leaf) {
         const int li = al.n_rl + __popc(mleaf & lt);
         if (li < kRlCap) {
-            s.rl[li] = w.v;
+            s.rl()[li] = w.v;
             child = ~li;
         } else {
             over = true;
@@ -161,15 +198,15 @@ __device__ __forceinline__ void place(bool have, int2 item, const Walk& w, int m
         const int p = __popc(mnode & lt);
         const int ri = al.n_rn + p, q2 = al.tail + 2 * p;
         if (p < node_room) {
-            s.rn[ri] = residue_node(w.feat == kFeatMem, w.v);
-            s.q[q2] = make_int2(w.aux, (ri * 2) | (tree << 16));
-            s.q[q2 + 1] = make_int2(w.aux + 1, (ri * 2 + 1) | (tree << 16));
+            s.rn()[ri] = residue_node(w.feat == kFeatMem, w.v);
+            s.q()[q2] = make_int2(w.aux, (ri * 2) | (tree << 16));
+            s.q()[q2 + 1] = make_int2(w.aux + 1, (ri * 2 + 1) | (tree << 16));
             child = ri;
         } else {
             over = true;
         }
     }
-    if (have && !over) reinterpret_cast<int*>(s.rn)[(dest >> 1) * 4 + 2 + (dest & 1)] = child;
+    if (have && !over) reinterpret_cast<int*>(s.rn())[(dest >> 1) * 4 + 2 + (dest & 1)] = child;
     al.fb_lo |= __reduce_or_sync(kFull, over && tree < 32 ? (1u << tree) : 0u);
     al.fb_hi |= __reduce_or_sync(kFull, over && tree >= 32 ? (1u << (tree - 32)) : 0u);
     al.n_rl += max(0, min(__popc(mleaf), kRlCap - al.n_rl));
@@ -193,8 +230,8 @@ __device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int 
     if (vb) b.n = __ldg(m.roots + t0 + 32 + lane);
     walk2(m.nodes, va, a, vb, b, row);
     const bool ca = va && a.feat != kFeatLeaf, cb = vb && b.feat != kFeatLeaf;
-    if (va && !ca) s.cval[lane] = a.v;
-    if (vb && !cb) s.cval[32 + lane] = b.v;
+    if (va && !ca) s.cval()[lane] = a.v;
+    if (vb && !cb) s.cval()[32 + lane] = b.v;
     const unsigned ma = __ballot_sync(kFull, ca), mb = __ballot_sync(kFull, cb);
     nonconst = static_cast<uint64_t>(ma) | (static_cast<uint64_t>(mb) << 32);
     fallback = 0u;
@@ -206,19 +243,19 @@ __device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int 
     al.fb_lo = al.fb_hi = 0u;
     if (ca) {
         const int idx = __popc(ma & lt);
-        s.rn[idx] = residue_node(a.feat == kFeatMem, a.v);
-        s.root[lane] = idx;
-        s.first[lane] = a.n;
-        s.q[2 * idx] = make_int2(a.aux, (idx * 2) | (lane << 16));
-        s.q[2 * idx + 1] = make_int2(a.aux + 1, (idx * 2 + 1) | (lane << 16));
+        s.rn()[idx] = residue_node(a.feat == kFeatMem, a.v);
+        s.root()[lane] = idx;
+        s.first()[lane] = a.n;
+        s.q()[2 * idx] = make_int2(a.aux, (idx * 2) | (lane << 16));
+        s.q()[2 * idx + 1] = make_int2(a.aux + 1, (idx * 2 + 1) | (lane << 16));
     }
     if (cb) {
         const int idx = __popc(ma) + __popc(mb & lt);
-        s.rn[idx] = residue_node(b.feat == kFeatMem, b.v);
-        s.root[32 + lane] = idx;
-        s.first[32 + lane] = b.n;
-        s.q[2 * idx] = make_int2(b.aux, (idx * 2) | ((32 + lane) << 16));
-        s.q[2 * idx + 1] = make_int2(b.aux + 1, (idx * 2 + 1) | ((32 + lane) << 16));
+        s.rn()[idx] = residue_node(b.feat == kFeatMem, b.v);
+        s.root()[32 + lane] = idx;
+        s.first()[32 + lane] = b.n;
+        s.q()[2 * idx] = make_int2(b.aux, (idx * 2) | ((32 + lane) << 16));
+        s.q()[2 * idx + 1] = make_int2(b.aux + 1, (idx * 2 + 1) | ((32 + lane) << 16));
     }
     __syncwarp();
     // Breadth-first rounds over the queue, two items per lane per iteration.
@@ -229,11 +266,11 @@ __device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int 
         const bool ha = qa < end, hb = qb < end;
         int2 ia = make_int2(0, 0), ib = make_int2(0, 0);
         if (ha) {
-            ia = s.q[qa];
+            ia = s.q()[qa];
             a.n = ia.x;
         }
         if (hb) {
-            ib = s.q[qb];
+            ib = s.q()[qb];
             b.n = ib.x;
         }
         walk2(m.nodes, ha, a, hb, b, row);
@@ -243,6 +280,42 @@ __device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int 
         __syncwarp();
     }
     fallback = static_cast<uint64_t>(al.fb_lo) | (static_cast<uint64_t>(al.fb_hi) << 32);
+    // Resolve each non-constant tree into a flat record (the queue is dead
+    // now; the key records alias it): lane l handles trees l and 32 + l.
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int t = lane + 32 * half;
+        if (t >= nt || !((nonconst >> t) & 1ull)) continue;
+        unsigned char type;
+        int4 key = make_int4(0, 0, 0, 0);
+        if ((fallback >> t) & 1ull) {
+            type = kFallbackTree;
+            key.x = s.first()[t];
+        } else {
+            const int4 r = s.rn()[s.root()[t]];
+            if (r.z < 0 && r.w < 0) {
+                type = r.x == -1 ? kSingleSm : kSingleMem;
+                s.cval()[t] = s.rl()[~r.z];
+                s.cv2()[t] = s.rl()[~r.w];
+                key = r;
+            } else {
+                const bool node_left = r.z >= 0;
+                const int4 c = s.rn()[node_left ? r.z : r.w];
+                if ((r.z < 0) != (r.w < 0) && c.z < 0 && c.w < 0) {
+                    type = node_left ? kDoubleLeft : kDoubleRight;
+                    s.cval()[t] = s.rl()[~(node_left ? r.w : r.z)];
+                    s.cv2()[t] = s.rl()[~c.z];
+                    s.cv3()[t] = s.rl()[~c.w];
+                    key = make_int4(r.x, r.y, c.x, c.y);
+                } else {
+                    type = kDagTree;
+                    key.x = s.root()[t];
+                }
+            }
+        }
+        s.ttype()[t] = type;
+        s.key()[t] = key;
+    }
 }
 
 // Full per-candidate traversal from node n (grid-variant nodes) with a packed
@@ -273,22 +346,25 @@ __device__ __forceinline__ void accumulate_model(const ModelRef& m, const double
             const int nth = min(32, nt - h);
             if (nth <= 0) break;
             const unsigned nc = static_cast<unsigned>(nonconst >> h);
-            const unsigned fbm = static_cast<unsigned>(fallback >> h);
             int jj = 0;
             while (jj < nth) {
                 // A run of constant trees jj .. jj+run-1, then one non-constant tree.
                 const unsigned rest = nc >> jj;
                 const int run = rest ? min(__ffs(rest) - 1, nth - jj) : nth - jj;
-                const double* cv = s.cval + h + jj;
+                const double* cv = s.cval() + h + jj;
                 int k = 0;
-                for (; k + 1 < run; k += 2) {
-                    const double v0 = cv[k], v1 = cv[k + 1];
+                for (; k + 3 < run; k += 4) {
+                    const double v0 = cv[k], v1 = cv[k + 1], v2 = cv[k + 2], v3 = cv[k + 3];
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v1);
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v2);
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v3);
                 }
-                if (k < run) {
+                for (; k < run; ++k) {
                     const double v0 = cv[k];
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
@@ -296,60 +372,50 @@ __device__ __forceinline__ void accumulate_model(const ModelRef& m, const double
                 jj += run;
                 if (jj >= nth) break;
                 const int j = h + jj;
-                const bool fb_tree = (fbm >> jj) & 1u;
                 ++jj;
-            if (fb_tree) {
-                const int32_t n = s.first[j];
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, n, row, ck[i]));
-            } else {
-                const int4 r = s.rn[s.root[j]];
-                const unsigned key = static_cast<unsigned>(r.y);
-                if (r.z < 0 && r.w < 0) {
+                const unsigned char type = s.ttype()[j];
+                const int4 kk = s.key()[j];
+                const unsigned rmask = static_cast<unsigned>(kk.x), rkey = static_cast<unsigned>(kk.y);
+                if (type == kSingleSm) {
                     // One clock test between two leaves: compare + select.
-                    const double lv = s.rl[~r.z], rv = s.rl[~r.w];
-                    if (r.x == -1) {
+                    const double lv = s.cval()[j], rv = s.cv2()[j];
 #pragma unroll
-                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= key ? lv : rv);
-                    } else {
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= rkey ? lv : rv);
+                } else if (type == kSingleMem) {
+                    const double lv = s.cval()[j], rv = s.cv2()[j];
 #pragma unroll
-                        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= key ? lv : rv);
-                    }
-                } else if ((r.z < 0) != (r.w < 0) && s.rn[r.z < 0 ? r.w : r.z].z < 0 &&
-                           s.rn[r.z < 0 ? r.w : r.z].w < 0) {
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= rkey ? lv : rv);
+                } else if (type == kDoubleLeft || type == kDoubleRight) {
                     // Two tests: the root and one child test, three leaves.
-                    const bool node_left = r.z >= 0;
-                    const int4 c = s.rn[node_left ? r.z : r.w];
-                    const double solo = s.rl[~(node_left ? r.w : r.z)];
-                    const double cl = s.rl[~c.z], cr = s.rl[~c.w];
-                    const unsigned rmask = static_cast<unsigned>(r.x), cmask = static_cast<unsigned>(c.x);
-                    const unsigned ckey = static_cast<unsigned>(c.y);
-                    if (node_left) {
+                    const double solo = s.cval()[j], cl = s.cv2()[j], cr = s.cv3()[j];
+                    const unsigned cmask = static_cast<unsigned>(kk.z), ckey = static_cast<unsigned>(kk.w);
+                    if (type == kDoubleLeft) {
 #pragma unroll
                         for (int i = 0; i < CPL; ++i) {
                             const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
-                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= key ? sub : solo);
+                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= rkey ? sub : solo);
                         }
                     } else {
 #pragma unroll
                         for (int i = 0; i < CPL; ++i) {
                             const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
-                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= key ? solo : sub);
+                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= rkey ? solo : sub);
                         }
                     }
-                } else {
+                } else if (type == kDagTree) {
 #pragma unroll
                     for (int i = 0; i < CPL; ++i) {
-                        int code = goes_left(r.x, r.y, ck[i]) ? r.z : r.w;
+                        int code = kk.x;
                         while (code >= 0) {
-                            const int4 q = s.rn[code];
+                            const int4 q = s.rn()[code];
                             code = goes_left(q.x, q.y, ck[i]) ? q.z : q.w;
                         }
-                        acc[i] = __dadd_rn(acc[i], s.rl[~code]);
+                        acc[i] = __dadd_rn(acc[i], s.rl()[~code]);
                     }
+                } else {  // kFallbackTree
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, kk.x, row, ck[i]));
                 }
-            }
             }
         }
         __syncwarp();
@@ -385,15 +451,9 @@ __global__ void __launch_bounds__(kThreads, (CPL >= 12 ? 4 : GD_GRID_MIN_BLOCKS)
     const int pair = warp >> 1;
     const bool is_time = warp & 1;
     const int F = p.n_cols;
-    unsigned char* base = smem + smem_per_warp(F) * warp;
     Scratch s;
-    s.row = reinterpret_cast<double*>(base);
-    s.cval = s.row + row_slots(F);
-    s.root = reinterpret_cast<int*>(s.cval + kChunk);
-    s.first = s.root + kChunk;
-    s.rn = reinterpret_cast<int4*>(s.first + kChunk);
-    s.rl = reinterpret_cast<double*>(s.rn + kRnCap);
-    s.q = reinterpret_cast<int2*>(s.rl + kRlCap);
+    s.base = smem + smem_per_warp(F) * warp;
+    double* const row = s.row();
     double* tbuf = reinterpret_cast<double*>(smem + smem_per_warp(F) * kWarps + smem_per_pair(CPL) * pair);
 
     unsigned ck[CPL];
@@ -418,14 +478,14 @@ __global__ void __launch_bounds__(kThreads, (CPL >= 12 ? 4 : GD_GRID_MIN_BLOCKS)
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
         __syncwarp();
         const double* src = p.rows + a * F;
-        for (int j = lane; j < F; j += 32) s.row[j] = __ldg(src + j);
+        for (int j = lane; j < F; j += 32) row[j] = __ldg(src + j);
         __syncwarp();
         if (is_time) {
             // the time model sees the time-encoded categorical columns
-            for (int k = lane; k < p.n_cat; k += 32) s.row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
+            for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
         }
-        accumulate_model<CPL>(m, s.row, sm_col, mem_col, s, ck, lane, acc);
+        accumulate_model<CPL>(m, row, sm_col, mem_col, s, ck, lane, acc);
         if (is_time) {
             pair_sync_a(pair);  // the energy warp is done reading the previous app's times
 #pragma unroll
@@ -526,9 +586,16 @@ int launch_cpl(const GridParams& p, bool general, int sm_count, cudaStream_t str
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    // Occupancy is set by registers (launch bounds); give shared memory the
-    // whole carveout so it never limits resident CTAs.
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    // Shared-memory carveout (percent of the unified L1/shared array).  The
+    // row-only walks read tree nodes through L1, so L1 capacity beats the
+    // last resident CTAs: measured on B200 (configs[1]) 80% -> 1.04 ms vs
+    // 100% -> 1.17 ms (all-constant trees: 0.40 vs 0.67 ms).
+    // GDVFS_CARVEOUT=<0..100> overrides (experiments).
+    static const int carveout = [] {
+        const char* e = std::getenv("GDVFS_CARVEOUT");
+        return e ? std::atoi(e) : 80;
+    }();
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
     const int blocks = grid_blocks(kWarps / 2, p.n_apps, sm_count, per_sm);
