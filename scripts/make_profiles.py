@@ -1,0 +1,86 @@
+#!/usr/bin/env python
+"""Copy the ncu / bench evidence of one GPU run from gpurun_out/ into profiles/.
+
+    python scripts/make_profiles.py <gpurun tag> <round tag>
+
+Writes profiles/<round>_launches.csv (per-kernel launch list: count, mean
+duration, DRAM bytes, share of GPU time), profiles/<round>_grid_kernel.txt
+(ncu --set full summary, per-source-line and per-opcode breakdown of the grid
+kernel), profiles/<round>_bench.json (both bench arms) and updates
+profiles/ncu_traffic.json (DRAM bytes per grid-kernel launch, read by
+bench.py for roofline.traffic).
+"""
+import collections
+import csv
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "gpurun_out"
+PROF = ROOT / "profiles"
+
+
+def launches(tag, rnd):
+    rows = [r for r in csv.DictReader(l for l in open(OUT / f"launches_{tag}.csv") if not l.startswith("=="))]
+    agg = collections.defaultdict(lambda: collections.defaultdict(float))
+    cnt = collections.Counter()
+    for r in rows:
+        k = r["Kernel Name"]
+        agg[k][r["Metric Name"]] += float(r["Metric Value"])
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            cnt[k] += 1
+    total = sum(v["gpu__time_duration.sum"] for v in agg.values())
+    with open(PROF / f"{rnd}_launches.csv", "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["kernel", "launches", "mean_duration_us", "dram_read_bytes_per_launch",
+                    "dram_write_bytes_per_launch", "share_of_gpu_time"])
+        for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"]):
+            n = cnt[k]
+            w.writerow([k[:110], n, round(v["gpu__time_duration.sum"] / n / 1e3, 2),
+                        int(v.get("dram__bytes_read.sum", 0) / n), int(v.get("dram__bytes_write.sum", 0) / n),
+                        round(v["gpu__time_duration.sum"] / total, 4)])
+    grid = {k: v for k, v in agg.items() if "grid_partial_kernel" in k}
+    traffic = None
+    for k, v in grid.items():
+        traffic = int((v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) / cnt[k])
+    return traffic
+
+
+def kernel_summary(tag, rnd):
+    rep = OUT / f"prof_grid_{tag}.ncu-rep"
+    parts = []
+    for cmd in (["python", "scripts/ncu_summary.py", str(rep), "--raw",
+                 r"dram__bytes_(read|write)\.sum$|lts__t_bytes\.sum$|l1tex__t_sector_hit_rate\.pct$|"
+                 r"smsp__inst_executed_pipe_fp64|sm__pipe_fp64_cycles_active"],
+                ["python", "scripts/ncu_lines.py", str(rep), "--top", "30"],
+                ["python", "scripts/ncu_sass.py", str(rep), "--top", "0"]):
+        parts.append("$ " + " ".join(cmd[1:]) + "\n" + subprocess.run(cmd, capture_output=True, text=True,
+                                                                          cwd=ROOT).stdout)
+    (PROF / f"{rnd}_grid_kernel.txt").write_text("\n".join(parts))
+
+
+def main():
+    tag, rnd = sys.argv[1], sys.argv[2]
+    PROF.mkdir(exist_ok=True)
+    traffic = launches(tag, rnd)
+    if (OUT / f"prof_grid_{tag}.ncu-rep").exists():
+        kernel_summary(tag, rnd)
+    bench = {}
+    for name in (f"bench_{tag}.json", f"bench_ref_{tag}.json"):
+        p = OUT / name
+        if p.exists() and p.read_text().strip():
+            bench[name] = json.loads(p.read_text().strip().splitlines()[-1])
+    if bench:
+        (PROF / f"{rnd}_bench.json").write_text(json.dumps(bench, indent=1))
+    if traffic is not None:
+        t = PROF / "ncu_traffic.json"
+        d = json.loads(t.read_text()) if t.exists() else {}
+        d["c2"] = traffic
+        t.write_text(json.dumps(d, indent=1))
+    print("traffic", traffic)
+
+
+if __name__ == "__main__":
+    main()
