@@ -7,6 +7,7 @@
 // missing/failed device is an error (GD_ERR_CUDA).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -87,7 +88,47 @@ int upload_model(gd_model* m) {
         int rc = gdh::pack_forest(v, m->n_cols, nodes, roots, m->max_depth);
         if (rc) return rc;
         m->packed_nodes = static_cast<int64_t>(nodes.size());
+        // Sentinel: tree t occupies packed nodes [roots[t], roots[t + 1]).
+        roots.push_back(static_cast<int32_t>(nodes.size()));
+        m->max_pair_nodes = 0;
+        m->max_tree_nodes = 0;
+        for (size_t t = 0; t + 1 < roots.size(); ++t) {
+            if (roots[t + 1] - roots[t] > m->max_tree_nodes) m->max_tree_nodes = roots[t + 1] - roots[t];
+        }
+        for (size_t t = 0; t + 1 < roots.size(); t += 2) {
+            const int32_t end = roots[t + 2 < roots.size() ? t + 2 : roots.size() - 1];
+            if (end - roots[t] > m->max_pair_nodes) m->max_pair_nodes = end - roots[t];
+        }
+        // Rank form (gd_device.cuh WNode): sorted distinct thresholds per
+        // feature and the walk-node tree offsets.
+        std::vector<std::vector<double>> per(static_cast<size_t>(m->n_cols));
+        for (const gd::PNode& x : nodes) {
+            if (x.feat >= 0 && x.v == x.v) per[static_cast<size_t>(x.feat)].push_back(x.v);
+        }
+        std::vector<double> thr;
+        std::vector<int32_t> thr_off(1, 0), wroots(1, 0);
+        m->max_thr_per_feature = 0;
+        for (auto& v : per) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end(), [](double a, double b) { return a == b; }), v.end());
+            thr.insert(thr.end(), v.begin(), v.end());
+            thr_off.push_back(static_cast<int32_t>(thr.size()));
+            if (static_cast<int32_t>(v.size()) > m->max_thr_per_feature) m->max_thr_per_feature = static_cast<int32_t>(v.size());
+        }
+        for (size_t t = 0; t + 1 < roots.size(); ++t) wroots.push_back(wroots.back() + ((roots[t + 1] - roots[t] + 1) & ~1));
+        m->n_wnodes = wroots.back();
         if (!m->ctx) return GD_OK;  // host-only model: validated, never uploaded
+        if (!thr.empty()) {
+            GD_CUDA(cudaMalloc(&m->d_thr, thr.size() * sizeof(double)), "cudaMalloc(thresholds)");
+            GD_CUDA(cudaMemcpy(m->d_thr, thr.data(), thr.size() * sizeof(double), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(thresholds)");
+        }
+        GD_CUDA(cudaMalloc(&m->d_thr_off, thr_off.size() * sizeof(int32_t)), "cudaMalloc(threshold offsets)");
+        GD_CUDA(cudaMemcpy(m->d_thr_off, thr_off.data(), thr_off.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                "cudaMemcpy(threshold offsets)");
+        GD_CUDA(cudaMalloc(&m->d_wroots, wroots.size() * sizeof(int32_t)), "cudaMalloc(walk roots)");
+        GD_CUDA(cudaMemcpy(m->d_wroots, wroots.data(), wroots.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                "cudaMemcpy(walk roots)");
         if (!nodes.empty()) {
             GD_CUDA(cudaMalloc(&m->d_nodes, nodes.size() * sizeof(gd::PNode)), "cudaMalloc(nodes)");
             GD_CUDA(cudaMemcpy(m->d_nodes, nodes.data(), nodes.size() * sizeof(gd::PNode), cudaMemcpyHostToDevice),
@@ -111,6 +152,14 @@ int upload_model(gd_model* m) {
 void release_model(gd_model* m) {
     if (m->d_grid_nodes) cudaFree(m->d_grid_nodes);
     m->d_grid_nodes = nullptr;
+    if (m->d_wnodes) cudaFree(m->d_wnodes);
+    m->d_wnodes = nullptr;
+    if (m->d_thr) cudaFree(m->d_thr);
+    if (m->d_thr_off) cudaFree(m->d_thr_off);
+    if (m->d_wroots) cudaFree(m->d_wroots);
+    m->d_thr = nullptr;
+    m->d_thr_off = nullptr;
+    m->d_wroots = nullptr;
     if (m->d_nodes) cudaFree(m->d_nodes);
     if (m->d_roots) cudaFree(m->d_roots);
     if (m->d_coef) cudaFree(m->d_coef);
@@ -184,9 +233,19 @@ int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t me
         GD_CUDA(cudaMalloc(&m->d_grid_nodes, static_cast<size_t>(m->packed_nodes) * sizeof(gd::PNode)),
                 "cudaMalloc(grid nodes)");
     }
+    if (!m->d_wnodes) {
+        GD_CUDA(cudaMalloc(&m->d_wnodes, static_cast<size_t>(m->n_wnodes) * sizeof(gd::WNode)),
+                "cudaMalloc(walk nodes)");
+    }
     int e = gd::launch_recode_clock_nodes(m->d_nodes, m->d_grid_nodes, m->packed_nodes, sm_col, mem_col, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "recode kernel");
+    GD_CUDA(cudaMemsetAsync(m->d_wnodes, 0, static_cast<size_t>(m->n_wnodes) * sizeof(gd::WNode), ctx->stream),
+            "memset(walk nodes)");
+    e = gd::launch_build_walk_nodes(m->d_grid_nodes, m->packed_nodes, m->d_roots, m->n_trees(), m->d_wroots,
+                                    m->d_thr, m->d_thr_off, m->d_wnodes, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "walk-node kernel");
     m->grid_sm_col = sm_col;
     m->grid_mem_col = mem_col;
     return GD_OK;
@@ -204,9 +263,21 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.e_nodes = general ? me->d_nodes : me->d_grid_nodes;
     p.e_roots = me->d_roots;
     p.e_trees = me->n_trees();
+    p.e_max_pair_nodes = me->max_pair_nodes;
+    p.t_max_pair_nodes = mt->max_pair_nodes;
+    p.max_tree_nodes = me->max_tree_nodes > mt->max_tree_nodes ? me->max_tree_nodes : mt->max_tree_nodes;
     p.e_base = me->base;
     p.e_lr = me->lr;
     p.t_nodes = general ? mt->d_nodes : mt->d_grid_nodes;
+    p.e_wnodes = me->d_wnodes;
+    p.t_wnodes = mt->d_wnodes;
+    p.e_wroots = me->d_wroots;
+    p.t_wroots = mt->d_wroots;
+    p.e_thr = me->d_thr;
+    p.t_thr = mt->d_thr;
+    p.e_thr_off = me->d_thr_off;
+    p.t_thr_off = mt->d_thr_off;
+    p.rank16 = me->max_thr_per_feature <= 65535 && mt->max_thr_per_feature <= 65535;
     p.t_roots = mt->d_roots;
     p.t_trees = mt->n_trees();
     p.t_base = mt->base;
@@ -232,8 +303,11 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.objective = o.objective;
     p.best_effort = o.best_effort;
     if (g.n_apps == 0) return GD_OK;
-    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream);
-    ++ctx->launches;
+    Scratch s{ctx->stream};
+    const size_t bytes = gd::grid_scratch_bytes(p, general);
+    const size_t i_scr = s.add(bytes);
+    GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
+    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches);
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");
     return GD_OK;
 }

@@ -49,6 +49,23 @@ __device__ __forceinline__ int thr_to_int(double thr) {
     return static_cast<int>(floor(thr));
 }
 
+__device__ __forceinline__ int clamp16(int t) { return min(max(t, 0), 65535); }
+
+// Key of a clock test: (double)clk <= thr  <=>  clk <= t16  for 1 <= clk <= 65535.
+__device__ __forceinline__ uint32_t t16_of(double thr) { return static_cast<uint32_t>(clamp16(thr_to_int(thr))); }
+
+// Number of sorted thresholds t[0..n) with t < x (NaN x: n).
+__device__ __forceinline__ int rank_of(const double* __restrict__ t, int n, double x) {
+    if (x != x) return n;
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(t + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // ---------------------------------------------------------------------------
 // Selection epilogue (K3).  Lane l owns the contiguous catalog clocks
 // l*CPL .. l*CPL+CPL-1, so lane-major order is catalog order.
@@ -93,10 +110,12 @@ __device__ __forceinline__ Cand shfl_cand(const Cand& c, int mask) {
     return o;
 }
 
+// cidx[i] = catalog index of this lane's slot i (-1 = empty).  Lane-major
+// slot order must be catalog order (literal mode scans it).
 template <int CPL>
 __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const double (&T)[CPL], const int (&smv)[CPL],
-                                                int lane, int n_clocks, double budget, int mode, int objective,
-                                                int best_effort, gd_decision* out) {
+                                                const int (&cidx)[CPL], int lane, double budget, int mode,
+                                                int objective, int best_effort, gd_decision* out) {
     Cand best;
     best.idx = -1;
     best.obj = best.t = best.e = 0.0;
@@ -104,8 +123,8 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
     if (mode == GD_MODE_TEXT) {
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-            const int c = lane * CPL + i;
-            if (c < n_clocks && !(T[i] > budget)) {
+            const int c = cidx[i];
+            if (c >= 0 && !(T[i] > budget)) {
                 Cand k{objective_value(E[i], T[i], objective), T[i], E[i], smv[i], c};
                 if (text_less(k, best)) best = k;
             }
@@ -121,13 +140,12 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
         // runs the same scan on broadcast values.
         double min_objective = DBL_MAX, max_time = budget;
         for (int l = 0; l < 32; ++l) {
-            if (l * CPL >= n_clocks) break;
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
-                const int c = l * CPL + i;
+                const int c = __shfl_sync(kFull, cidx[i], l);
                 const double e = __shfl_sync(kFull, E[i], l);
                 const double t = __shfl_sync(kFull, T[i], l);
-                if (c >= n_clocks) continue;
+                if (c < 0) continue;
                 const double value = objective_value(e, t, objective);
                 if (value < min_objective && t <= max_time) {
                     min_objective = value;
@@ -143,8 +161,8 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
     if (best.idx < 0 && best_effort) {
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
-            const int c = lane * CPL + i;
-            if (c < n_clocks) {
+            const int c = cidx[i];
+            if (c >= 0) {
                 Cand k{0.0, T[i], E[i], smv[i], c};
                 if (fast_less(k, best)) best = k;
             }
@@ -165,6 +183,13 @@ __device__ __forceinline__ void select_epilogue(const double (&E)[CPL], const do
         d.time_s = best.idx >= 0 ? best.t : 0.0;
         *out = d;
     }
+}
+
+// Contiguous slot map: lane l owns catalog clocks l*CPL .. l*CPL+CPL-1.
+template <int CPL>
+__device__ __forceinline__ void contiguous_cidx(int lane, int n_clocks, int (&cidx)[CPL]) {
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) cidx[i] = lane * CPL + i < n_clocks ? lane * CPL + i : -1;
 }
 
 // Full per-candidate traversal from node n (row + clock override): the

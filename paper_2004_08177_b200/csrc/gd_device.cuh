@@ -9,6 +9,7 @@
 //             models.cpp:71-78) so leaf ids come out in the caller's numbering.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include "gdvfs.h"
@@ -22,6 +23,21 @@ struct __align__(16) PNode {
 };
 static_assert(sizeof(PNode) == 16, "PNode must stay 16 bytes");
 
+// Walk node (8 bytes), the rank form of a grid node used by the walk kernel:
+//   internal: key = index of its threshold among the sorted distinct non-NaN
+//             thresholds of its feature (-1 for a NaN threshold);
+//   clock:    key = t16 (clamp(floor(thr), 0, 65535));
+//   leaf:     key = packed (grid) index of the leaf;
+//   fc = feat << 16 | child: feat (signed; kFeat* for leaf / clock) in the
+//   high half, the tree-local index of the left child (right = child + 1) in
+//   the low half.  With rank(x) = #{thresholds of the feature < x} (NaN x:
+//   their count), `x <= thr_k  <=>  rank(x) <= k` exactly.
+struct __align__(8) WNode {
+    int32_t key;
+    int32_t fc;
+};
+static_assert(sizeof(WNode) == 8, "WNode must stay 8 bytes");
+
 // In the grid variant of a packed model the clock columns are recoded so one
 // `feat < 0` test stops a row-only walk: leaf -1, sm_clock -2, mem_clock -3.
 constexpr int32_t kFeatLeaf = -1;
@@ -34,8 +50,19 @@ struct GridParams {
     const int32_t* e_roots;
     const PNode* t_nodes;
     const int32_t* t_roots;
+    const WNode* e_wnodes;  // walk nodes (rank form), trees padded to an even node count
+    const WNode* t_wnodes;
+    const int32_t* e_wroots;  // n_trees + 1, in walk-node units
+    const int32_t* t_wroots;
+    const double* e_thr;      // sorted distinct thresholds per feature, [thr_off[f], thr_off[f+1])
+    const double* t_thr;
+    const int32_t* e_thr_off;
+    const int32_t* t_thr_off;
     double e_base, e_lr, t_base, t_lr;
     int32_t e_trees, t_trees;
+    int32_t e_max_pair_nodes, t_max_pair_nodes;  // roots[] carry a sentinel roots[n_trees]
+    int32_t max_tree_nodes;
+    int32_t rank16;  // every feature has <= 65535 distinct thresholds (16-bit ranks)
 
     const double* rows;    // [n_records, n_cols] energy-encoded
     const double* rows_t;  // [n_records, n_cols] time-encoded (general mode only)
@@ -73,11 +100,23 @@ int launch_predict_linear(const double* coef, double intercept, int clamp, const
                           int32_t n_cols, double* out, int sm_count, void* stream);
 int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* cat_cols, int32_t n_cat,
                         int64_t n_records, int32_t n_cols, double* rows_t, void* stream);
-int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream);
+// The grid path (gd_grid.cu).  Without rec_of_clock it runs, per app batch,
+// the walk kernel then the accumulate+select kernel, using `scratch` (at
+// least grid_scratch_bytes) for the per-(app, tree) records; `launches` is
+// incremented per kernel launched.
+int64_t grid_scratch_per_app(const GridParams& p);
+size_t grid_scratch_bytes(const GridParams& p, bool general);
+int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
+                       size_t scratch_bytes, int64_t* launches);
 int launch_select(const SelectParams& p, int sm_count, void* stream);
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
 // Copy `n` packed nodes recoding features sm_col / mem_col as kFeatSm / kFeatMem.
 int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t sm_col, int32_t mem_col, void* stream);
+
+// Walk nodes (rank form) from grid nodes; `dst` must be zeroed (padding).
+int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
+                            const int32_t* wroots, const double* thr, const int32_t* thr_off, WNode* dst,
+                            void* stream);
 
 // Largest clock catalog the fused kernels take (32 lanes x 16 clocks).
 constexpr int kMaxClocks = 512;

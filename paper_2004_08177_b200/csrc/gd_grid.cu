@@ -1,33 +1,35 @@
-// gd_grid.cu -- K2+K3: the fused (app x clock) grid kernel.
+// gd_grid.cu -- K2+K3: the (app x clock) grid path.
 //
 // Replaces ModelPredictorState::build + 2x models::predict
 // (scheduler.cpp:329-370) and decide()'s selection (scheduler.cpp:54-100,
 // 187-234): candidate rows are never materialised, both ensembles are
 // evaluated for every catalog clock of an app, and the deadline-masked
-// selection runs in the same CTA.
-//
-// Work split.  A warp PAIR owns one app at a time: the even warp evaluates
-// the energy ensemble, the odd warp the time ensemble, each lane owning the
-// contiguous catalog clocks l*CPL .. l*CPL+CPL-1 (one in-order accumulator
-// per clock).  The time warp hands its CPL times per lane to the energy warp
-// through shared memory (two named barriers per app); the energy warp runs
-// the selection epilogue.
+// selection runs in the epilogue.
 //
 // Partial evaluation.  For one app every candidate row is identical except
 // the sm_clock / mem_clock columns, so every non-clock node test has the same
-// outcome for all C clocks.  Per chunk of 32 trees a warp
-//   phase 1 (lane per work item): walks each tree's row-only path from the
-//     root; a path ending on a leaf is a constant for all C clocks.  A path
-//     ending on a clock node becomes a residue node and queues its two
-//     children, walked the same way in later rounds -- a warp-wide
-//     breadth-first expansion with ballot-prefix allocation (no atomics, no
-//     per-lane stacks);
-//   phase 2 (lane per clock range): adds, in tree order, the constant or the
-//     residue's leaf to each owned accumulator with __dadd_rn.  A residue
-//     that is one test between two leaves (the common case) is evaluated
-//     branch-free with one compare + select per clock.
-// The leaf each candidate reaches is exactly predict_row's leaf
-// (models.cpp:71-78), so the ordered sums are bit-identical.
+// outcome for all C clocks.  A tree therefore contributes, per app, either a
+// constant (its row-only walk ends on a leaf) or a small clock-only residue
+// (the walk stops at a clock node; below it, row-only walks again end on
+// leaves or further clock nodes).  The leaf each candidate reaches is exactly
+// predict_row's leaf (models.cpp:71-78), so the ordered sums are bit-exact.
+//
+// Two kernels per app batch:
+//
+//   K2a grid_walk_kernel  (tree-major, latency / L1 bound)
+//       lanes = 32 apps, every warp of a CTA walks the same trees, so node
+//       loads coalesce at the top levels and hit L1 below; app rows are
+//       staged in shared memory.  Each (app, tree) is resolved into one
+//       16-byte TreeRec: CONST (leaf value), SM / MEM (one clock test between
+//       two leaves), T2 (<= 3 tests, 4 leaves; 48-byte side record) or FULL
+//       (anything deeper: per-clock traversal from the first clock node).
+//   K2b grid_acc_kernel   (app-major, FP64-add / issue bound)
+//       a warp PAIR per app (energy warp, time warp), lane l owning the
+//       contiguous catalog clocks l*CPL .. l*CPL+CPL-1 (one in-order
+//       accumulator per clock).  The app's records stream through a
+//       cp.async ring (32 trees per stage, side data one stage behind), and
+//       every record becomes CPL __dadd_rn's in tree order.  The energy warp
+//       then runs the selection epilogue (K3) on the pair's E/T values.
 //
 // Clock packing.  Each owned clock is one register ck = sm << 16 | mem
 // (1 <= sm, mem <= 65535, validated on the host).  A test `(double)sm <= thr`
@@ -42,284 +44,629 @@ namespace {
 
 using namespace dev;
 
-// Resident CTAs per SM the partial kernel is compiled for (register cap
-// 65536 / (128 * N)); 8 -> 64 registers, 32 warps per SM.
-#ifndef GD_GRID_MIN_BLOCKS
-#define GD_GRID_MIN_BLOCKS 8
-#endif
+// ---------------------------------------------------------------------------
+// The walk -> accumulate hand-off.
+// ---------------------------------------------------------------------------
+enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4 };
 
-constexpr int kWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
-constexpr int kThreads = kWarps * 32;
-constexpr int kChunk = 64;         // trees per chunk: two independent root walks per lane
-constexpr int kRnCap = 64;         // residue clock nodes per warp per chunk (>= kChunk)
-constexpr int kRlCap = 128;        // residue leaves per warp per chunk
-constexpr int kQCap = 2 * kRnCap;  // queued walks (two per residue node)
+// One (app, tree) record.  info = kind | t16 << 16 (SM / MEM keys).
+//   CONST: v = leaf value.              SM/MEM: v = left leaf, ref = right leaf node.
+//   TABLE: ref = residue-table index.   FULL:   ref = first clock node.
+struct __align__(16) TreeRec {
+    double v;
+    uint32_t info;
+    int32_t ref;
+};
+static_assert(sizeof(TreeRec) == 16, "TreeRec is 16 bytes");
 
-// Per warp: row[F] | cval, cv2, cv3 [64] | root, first [64] | ttype[64] |
-// rn[kRnCap] | rl[kRlCap] | q[kQCap] (the per-tree key records alias q once
-// the expansion is done).  The row is padded to an even number of doubles so
-// every later array is 16-B aligned.
-__host__ __device__ constexpr int row_slots(int n_cols) { return (n_cols + 1) & ~1; }
-// Fixed byte offsets inside a warp's region (the row, whose size depends on
-// the column count, goes last) so every array is base + constant: one live
-// register instead of one pointer per array.
-constexpr int kOffCval = 0;
-constexpr int kOffCv2 = kOffCval + kChunk * 8;
-constexpr int kOffCv3 = kOffCv2 + kChunk * 8;
-constexpr int kOffRn = kOffCv3 + kChunk * 8;
-constexpr int kOffRl = kOffRn + kRnCap * 16;
-constexpr int kOffQ = kOffRl + kRlCap * 8;
-constexpr int kOffRoot = kOffQ + kQCap * 8;
-constexpr int kOffFirst = kOffRoot + kChunk * 4;
-constexpr int kOffType = kOffFirst + kChunk * 4;
-constexpr int kOffRow = (kOffType + kChunk + 15) & ~15;
-__host__ __device__ constexpr size_t smem_per_warp(int n_cols) {
-    return static_cast<size_t>(kOffRow) + static_cast<size_t>(row_slots(n_cols)) * 8;
+// A residue table: the clock-only residue of one (app, tree) as a balanced
+// tree of depth D (2 or 3).  Test k is node k (children 2k+1, 2k+2); a clock
+// goes right iff (ck & mask) > key (always-left = {0, 0}); leaf l is node
+// 2^D - 1 + l.
+struct __align__(16) RTRec {
+    uint2 test[7];
+    uint32_t depth;
+    uint32_t pad;
+    double leaf[8];
+};
+static_assert(sizeof(RTRec) == 128, "RTRec is 128 bytes");
+
+
+// Records of tree t for batch-local app la: pairs of trees are interleaved
+// per app so a lane of the walk kernel stores 32 contiguous bytes.
+__host__ __device__ __forceinline__ int64_t rec_index(int32_t t, int64_t la, int64_t n_apps) {
+    return ((static_cast<int64_t>(t >> 1) * n_apps + la) << 1) | (t & 1);
 }
-static_assert(kQCap * 8 >= kChunk * 16, "key records alias the queue");
-// Per pair: the time warp's T values, 32 lanes x CPL.
-__host__ __device__ constexpr size_t smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
 
-// Per-tree residue classes resolved after the expansion (phase 2 dispatch).
-enum : unsigned char {
-    kConstTree = 0,
-    kSingleSm = 1,    // cval / cv2 = left / right leaf, key.y = key
-    kSingleMem = 2,
-    kDoubleLeft = 3,  // root test, node child on the left: cval = right leaf,
-    kDoubleRight = 4, //   cv2 / cv3 = child's left / right leaf, key = {rmask, rkey, cmask, ckey}
-    kDagTree = 5,     // key.x = residue root
-    kFallbackTree = 6 // key.x = first clock node
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+struct AccParams {
+    const PNode* nodes[2];
+    int32_t n_trees[2];
+    double base[2], lr[2];
+    const TreeRec* rec[2];
+    const RTRec* pool;
+    const double* rows;
+    const double* cat_t;
+    const int32_t* cat_cols;
+    const int32_t* sm;
+    const int32_t* mem;
+    const double* budgets;
+    gd_decision* out;
+    double* e_out;
+    double* t_out;
+    int64_t a0;
+    int32_t n_apps;
+    int32_t n_cols, n_cat, n_clocks;
+    int32_t mode, objective, best_effort;
 };
 
-struct Scratch {
-    unsigned char* base;  // this warp's region
-    // constant leaf per tree of the chunk / record value 0
-    __device__ __forceinline__ double* cval() const { return reinterpret_cast<double*>(base + kOffCval); }
-    __device__ __forceinline__ double* cv2() const { return reinterpret_cast<double*>(base + kOffCv2); }
-    __device__ __forceinline__ double* cv3() const { return reinterpret_cast<double*>(base + kOffCv3); }
-    // residue nodes {and-mask, packed key, lo code, hi code}; code < 0: ~leaf slot
-    __device__ __forceinline__ int4* rn() const { return reinterpret_cast<int4*>(base + kOffRn); }
-    __device__ __forceinline__ double* rl() const { return reinterpret_cast<double*>(base + kOffRl); }
-    // queued walks {node, dest (rn*2 + side) | tree << 16}
-    __device__ __forceinline__ int2* q() const { return reinterpret_cast<int2*>(base + kOffQ); }
-    // per-tree key records (alias the queue once the expansion is done)
-    __device__ __forceinline__ int4* key() const { return reinterpret_cast<int4*>(base + kOffQ); }
-    __device__ __forceinline__ int* root() const { return reinterpret_cast<int*>(base + kOffRoot); }
-    __device__ __forceinline__ int* first() const { return reinterpret_cast<int*>(base + kOffFirst); }
-    __device__ __forceinline__ unsigned char* ttype() const { return base + kOffType; }
-    __device__ __forceinline__ double* row() const { return reinterpret_cast<double*>(base + kOffRow); }
+struct WalkParams {
+    const WNode* wnodes[2];
+    const int32_t* wroots[2];  // n_trees + 1 entries, walk-node units
+    const int32_t* roots[2];   // grid roots, n_trees + 1 entries
+    const PNode* gnodes[2];    // grid nodes (leaf values)
+    int32_t n_trees[2];
+    const uint16_t* ranks;     // [2][n_apps][n_cols] for the batch
+    int32_t n_apps;            // apps in the batch
+    int32_t n_cols;
+    int32_t tile_apps;         // apps per work item = 32 * groups
+    int32_t splits;            // tree-pair ranges per model
+    int32_t n_items;           // tiles * 2 * splits, tile-major
+    int32_t win_nodes;         // per-tree window staged in shared memory (BFS prefix, even)
+    int32_t stage_nodes;       // capacity of one stage buffer (walk nodes)
+    TreeRec* rec[2];
+    RTRec* pool;
+    uint32_t* pool_count;
+    uint32_t pool_cap;
 };
 
-struct ModelRef {
+// ---------------------------------------------------------------------------
+// K2a: walks.
+//
+// Persistent CTAs, each owning a contiguous range of work items (app tile x
+// model x tree-pair range).  A stage is a run of consecutive tree pairs whose
+// top-level windows (the first win_nodes walk nodes of each tree: its top
+// levels, trees being laid out breadth-first) fit one shared-memory buffer;
+// thread 0 streams the next stage in with TMA bulk copies (cp.async.bulk +
+// mbarrier) while the CTA walks the current one.  Rows are staged as 16-bit
+// feature ranks, transposed ([col][app]) so lane-per-app reads are
+// conflict-free; walks compare ranks with threshold indices (WNode).
+// ---------------------------------------------------------------------------
+
+struct Walk {
+    int32_t n;    // tree-local node index
+    int32_t key;
+    int32_t fc;   // feat << 16 | child
+};
+
+__device__ __forceinline__ int32_t wfeat(int32_t fc) { return fc >> 16; }
+__device__ __forceinline__ int32_t wchild(int32_t fc) { return fc & 0xffff; }
+
+// Where one tree's walk nodes live during a stage.
+struct TreeSrc {
+    int32_t wroot;    // walk-node index of the root
+    int32_t groot;    // grid index of the root
+    uint32_t win;     // nodes [0, win) of the tree are in shared memory ...
+    uint32_t saddr;   // ... at this shared address
+};
+
+struct WalkCtx {
+    const WNode* __restrict__ wnodes;  // global walk nodes of the model
+    const PNode* __restrict__ gnodes;  // grid nodes (leaf values)
+    uint32_t row_saddr;                // shared address of this lane's app in the staged ranks
+    int32_t row_stride;                // bytes between consecutive columns
+};
+
+template <bool kAllSmem>
+__device__ __forceinline__ void load_wnode(const WalkCtx& c, const TreeSrc& s, Walk& w) {
+    if (kAllSmem || static_cast<uint32_t>(w.n) < s.win) {
+        asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
+                     : "=r"(w.key), "=r"(w.fc)
+                     : "r"(s.saddr + static_cast<uint32_t>(w.n) * 8u));
+    } else {
+        const int2 q = __ldg(reinterpret_cast<const int2*>(c.wnodes + s.wroot + w.n));
+        w.key = q.x;
+        w.fc = q.y;
+    }
+}
+
+__device__ __forceinline__ int32_t rank_value(const WalkCtx& c, int32_t fc) {
+    uint16_t x;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(c.row_saddr + static_cast<uint32_t>(wfeat(fc) * c.row_stride)));
+    return static_cast<int32_t>(x);
+}
+
+// N independent row-only walks advanced in lockstep until each reaches a leaf
+// or a clock node (feat < 0, i.e. fc < 0).  Invalid walks only load their
+// start node.
+template <bool kAllSmem, int N>
+__device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], const bool (&v)[N], Walk (&w)[N]) {
+    bool g[N];
+    bool any = false;
+#pragma unroll
+    for (int h = 0; h < N; ++h) {
+        load_wnode<kAllSmem>(c, s[h], w[h]);
+        g[h] = v[h] && w[h].fc >= 0;
+        any |= g[h];
+    }
+    while (any) {
+        int32_t x[N];
+#pragma unroll
+        for (int h = 0; h < N; ++h) x[h] = rank_value(c, g[h] ? w[h].fc : 0);
+        any = false;
+#pragma unroll
+        for (int h = 0; h < N; ++h) {
+            const int32_t nn = wchild(w[h].fc) + (x[h] <= w[h].key ? 0 : 1);
+            w[h].n = g[h] ? nn : w[h].n;
+            load_wnode<kAllSmem>(c, s[h], w[h]);
+            g[h] = g[h] && w[h].fc >= 0;
+            any |= g[h];
+        }
+    }
+}
+
+template <bool kAllSmem>
+__device__ __forceinline__ void walk2(const WalkCtx& c, const TreeSrc& s, bool va, Walk& a, bool vb, Walk& b) {
+    const TreeSrc ss[2] = {s, s};
+    const bool vv[2] = {va, vb};
+    Walk ww[2] = {a, b};
+    walkn<kAllSmem, 2>(c, ss, vv, ww);
+    a = ww[0];
+    b = ww[1];
+}
+
+// Compare key of a clock node's test (see the header comment).
+__device__ __forceinline__ uint2 test_mk(const Walk& w) {
+    const uint32_t t = static_cast<uint32_t>(w.key);
+    return wfeat(w.fc) == kFeatMem ? make_uint2(0xffffu, t) : make_uint2(0xffffffffu, (t << 16) | 0xffffu);
+}
+
+__device__ __forceinline__ double leaf_value(const WalkCtx& c, const Walk& w) { return __ldg(&c.gnodes[w.key].v); }
+
+__device__ __forceinline__ Walk child_walk(const Walk& w, int side) { return Walk{wchild(w.fc) + side, 0, 0}; }
+
+// Resolve a tree whose root walk stopped at clock node `w` into its record:
+// one test between two leaves -> SM / MEM; a residue of depth <= 3 -> a
+// residue table (balanced; a leaf above the last level is replicated under
+// always-left tests); deeper -> FULL.
+template <bool kAllSmem>
+__device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const WalkCtx& c, const TreeSrc& s,
+                                                   const Walk& w) {
+    TreeRec r;
+    r.v = 0.0;
+    Walk A = child_walk(w, 0), B = child_walk(w, 1);
+    walk2<kAllSmem>(c, s, true, A, true, B);
+    const bool ac = A.fc < 0 && wfeat(A.fc) != kFeatLeaf, bc = B.fc < 0 && wfeat(B.fc) != kFeatLeaf;
+    if (!ac && !bc) {
+        r.v = leaf_value(c, A);
+        r.info = (wfeat(w.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w.key) << 16);
+        r.ref = B.key;
+        return r;
+    }
+    r.info = kRecFull;
+    r.ref = s.groot + w.n;
+    const uint32_t idx = atomicAdd(p.pool_count, 1u);
+    if (idx >= p.pool_cap) return r;
+    RTRec* q = p.pool + idx;
+    const uint2 left = make_uint2(0u, 0u);
+    Walk X[4] = {A, A, B, B};
+    if (ac) {
+        X[0] = child_walk(A, 0);
+        X[1] = child_walk(A, 1);
+    }
+    if (bc) {
+        X[2] = child_walk(B, 0);
+        X[3] = child_walk(B, 1);
+    }
+    walk2<kAllSmem>(c, s, ac, X[0], ac, X[1]);
+    walk2<kAllSmem>(c, s, bc, X[2], bc, X[3]);
+    q->test[0] = test_mk(w);
+    q->test[1] = ac ? test_mk(A) : left;
+    q->test[2] = bc ? test_mk(B) : left;
+    bool deeper = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) deeper |= wfeat(X[k].fc) != kFeatLeaf;
+    if (!deeper) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q->leaf[k] = leaf_value(c, X[k]);
+        q->depth = 2;
+        r.info = kRecTable;
+        r.ref = static_cast<int32_t>(idx);
+        return r;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool xc = wfeat(X[k].fc) != kFeatLeaf;
+        q->test[3 + k] = xc ? test_mk(X[k]) : left;
+        Walk L = X[k], R = X[k];
+        if (xc) {
+            L = child_walk(X[k], 0);
+            R = child_walk(X[k], 1);
+        }
+        walk2<kAllSmem>(c, s, xc, L, xc, R);
+        if (wfeat(L.fc) != kFeatLeaf || wfeat(R.fc) != kFeatLeaf) return r;  // deeper than 3: FULL
+        q->leaf[2 * k] = leaf_value(c, L);
+        q->leaf[2 * k + 1] = leaf_value(c, R);
+    }
+    q->depth = 3;
+    r.info = kRecTable;
+    r.ref = static_cast<int32_t>(idx);
+    return r;
+}
+
+// A root walk that stopped at a clock node, queued for resolution so the
+// (divergent) residue walks run with full warps.
+struct Job {
+    int32_t n;       // the clock node (tree-local index)
+    int32_t t;       // tree
+    uint32_t saddr;  // shared address of the tree's window
+    int32_t li;      // app within the tile
+};
+constexpr int kJobCap = 64;
+
+// Lanes take queued jobs [0, min(32, count)) and write their records, then
+// the queue's tail moves to the front.
+template <bool kAllSmem>
+__device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, Job* jobs, int& count, int lane,
+                                         int model, TreeRec* out, int64_t tile0) {
+    const int take = min(32, count);
+    if (lane < take) {
+        const Job j = jobs[lane];
+        WalkCtx c = c0;
+        c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * 2);
+        TreeSrc s;
+        s.wroot = __ldg(p.wroots[model] + j.t);
+        s.groot = __ldg(p.roots[model] + j.t);
+        s.win = kAllSmem ? 0xffffffffu
+                         : static_cast<uint32_t>(min(__ldg(p.wroots[model] + j.t + 1) - s.wroot, p.win_nodes));
+        s.saddr = j.saddr;
+        Walk w{j.n, 0, 0};
+        load_wnode<kAllSmem>(c, s, w);
+        out[rec_index(j.t, tile0 + j.li, p.n_apps)] = resolve_residue<kAllSmem>(p, c, s, w);
+    }
+    __syncwarp();
+    const int rest = count - take;
+    Job mv;
+    if (lane < rest) mv = jobs[take + lane];
+    __syncwarp();
+    if (lane < rest) jobs[lane] = mv;
+    __syncwarp();
+    count = rest;
+}
+
+// Queue the walk of one tree if it stopped at a clock node, else store its
+// constant record; run a round of jobs once 32 are pending.
+template <bool kAllSmem>
+__device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const WalkCtx& c, Job* jobs,
+                                            int& count, int lane, bool v, const Walk& w, int32_t t, uint32_t saddr,
+                                            int li, int model, TreeRec* out, int64_t tile0) {
+    const bool job = v && wfeat(w.fc) != kFeatLeaf;
+    if (v && !job) {
+        TreeRec r;
+        r.v = leaf_value(c, w);
+        r.info = kRecConst;
+        r.ref = 0;
+        out[rec_index(t, tile0 + li, p.n_apps)] = r;
+    }
+    const unsigned m = __ballot_sync(kFull, job);
+    if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, saddr, li};
+    count += __popc(m);
+    __syncwarp();
+    if (count >= 32) run_jobs<kAllSmem>(p, c0, jobs, count, lane, model, out, tile0);
+}
+
+constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
+
+// One stage of the CTA's schedule.
+struct Stage {
+    int32_t item, q0, q1, valid;
+};
+
+struct ItemInfo {
+    int32_t tile, model, p0, p1;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const WalkParams& p, int32_t it) {
+    ItemInfo r;
+    const int32_t per_tile = 2 * p.splits;
+    r.tile = it / per_tile;
+    const int32_t k = it - r.tile * per_tile;
+    r.model = k / p.splits;
+    const int32_t split = k - r.model * p.splits;
+    const int64_t pairs = (p.n_trees[r.model] + 1) >> 1;
+    r.p0 = static_cast<int32_t>(pairs * split / p.splits);
+    r.p1 = static_cast<int32_t>(pairs * (split + 1) / p.splits);
+    return r;
+}
+
+__device__ __forceinline__ int32_t tree_window(const WalkParams& p, const int32_t* wroots, int32_t t) {
+    return min(__ldg(wroots + t + 1) - __ldg(wroots + t), p.win_nodes);
+}
+
+// Thread 0: the next stage after cursor (it, q), advancing the cursor.
+__device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q) {
+    Stage s{0, 0, 0, 0};
+    while (it < it_end) {
+        const ItemInfo ii = item_info(p, it);
+        if (q < ii.p0) q = ii.p0;
+        if (q >= ii.p1) {
+            ++it;
+            q = -1;
+            continue;
+        }
+        const int32_t nt = p.n_trees[ii.model];
+        const int32_t* wroots = p.wroots[ii.model];
+        int32_t used = 0, qe = q;
+        while (qe < ii.p1) {
+            int32_t w = tree_window(p, wroots, 2 * qe);
+            if (2 * qe + 1 < nt) w += tree_window(p, wroots, 2 * qe + 1);
+            if (qe > q && (used + w > p.stage_nodes || 2 * (qe - q + 1) > kStageTrees)) break;
+            used += w;
+            ++qe;
+        }
+        s = Stage{it, q, qe, 1};
+        q = qe;
+        return s;
+    }
+    return s;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// Thread 0: load the windows of stage s into buffer `buf` (adjacent whole
+// trees in one bulk copy), arm its barrier and fill the stage's tree table
+// {walk root, grid root, window nodes, shared address}.
+__device__ void issue_stage(const WalkParams& p, const Stage& s, uint32_t buf_saddr, uint32_t bar, int4* table) {
+    const ItemInfo ii = item_info(p, s.item);
+    const int32_t nt = p.n_trees[ii.model];
+    const int32_t* wroots = p.wroots[ii.model];
+    const int32_t* roots = p.roots[ii.model];
+    const WNode* nodes = p.wnodes[ii.model];
+    uint32_t bytes = 0;
+    for (int32_t t = 2 * s.q0; t < 2 * s.q1 && t < nt; ++t) bytes += 8u * tree_window(p, wroots, t);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    uint32_t off = 0, run = 0;
+    const WNode* run_src = nullptr;
+    for (int32_t t = 2 * s.q0; t < 2 * s.q1 && t < nt; ++t) {
+        const int32_t wr = __ldg(wroots + t);
+        const int32_t win = tree_window(p, wroots, t);
+        const uint32_t w = 8u * static_cast<uint32_t>(win);
+        const WNode* src = nodes + wr;
+        if (run > 0 && reinterpret_cast<const char*>(run_src) + run != reinterpret_cast<const char*>(src)) {
+            bulk_g2s(buf_saddr + off - run, run_src, run, bar);
+            run = 0;
+        }
+        if (run == 0) run_src = src;
+        table[t - 2 * s.q0] = make_int4(wr, __ldg(roots + t), win, static_cast<int>(buf_saddr + off));
+        run += w;
+        off += w;
+    }
+    if (run > 0) bulk_g2s(buf_saddr + off - run, run_src, run, bar);
+}
+
+// Shared layout: barriers + stage descriptors | buffer 0 | buffer 1 | ranks
+// [n_cols][tile_apps] u16 | per-warp job queues | stage tree tables.
+__host__ __device__ constexpr size_t walk_jobs_bytes(int warps) {
+    return static_cast<size_t>(warps) * kJobCap * sizeof(Job);
+}
+__host__ __device__ constexpr size_t walk_rank_bytes(int n_cols, int tile_apps) {
+    return (static_cast<size_t>(n_cols) * tile_apps * 2 + 15) & ~static_cast<size_t>(15);
+}
+
+// Grid: persistent CTAs; blockDim = 64 * groups (two warps per group of 32
+// apps, taking the even / odd trees of every stage).
+template <bool kAllSmem>
+__global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant__ WalkParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TA = p.tile_apps, groups = TA >> 5;
+    const int group = warp % groups, sub = warp / groups;
+    const size_t buf_bytes = static_cast<size_t>(p.stage_nodes) * 8;
+    Stage* desc = reinterpret_cast<Stage*>(smem + 16);
+    const uint32_t bar0 = smem_addr(smem), bufs0 = smem_addr(smem + 128);
+    uint16_t* srank = reinterpret_cast<uint16_t*>(smem + 128 + 2 * buf_bytes);
+    unsigned char* after_ranks = smem + 128 + 2 * buf_bytes + walk_rank_bytes(p.n_cols, TA);
+    Job* jobs = reinterpret_cast<Job*>(after_ranks) + warp * kJobCap;
+    int4* tables = reinterpret_cast<int4*>(after_ranks + walk_jobs_bytes(blockDim.x >> 5));
+    const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
+    const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
+
+    int32_t cur_it = it_begin, cur_q = -1;  // thread 0's schedule cursor
+    if (threadIdx.x == 0) {
+        mbar_init(bar0, 1);
+        mbar_init(bar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const Stage s = next_stage(p, it_end, cur_it, cur_q);
+        desc[0] = s;
+        if (s.valid) issue_stage(p, s, bufs0, bar0, tables);
+    }
+    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    int32_t row_tile = -1, row_model = -1;
+    for (int k = 0;; ++k) {
+        const int buf = k & 1;
+        __syncthreads();  // stage k-1 is done: buffer buf ^ 1 and its table are free
+        const Stage s = desc[buf];
+        if (!s.valid) break;
+        if (threadIdx.x == 0) {
+            // Plan and load stage k + 1 while the CTA walks stage k.
+            const Stage nx = next_stage(p, it_end, cur_it, cur_q);
+            desc[buf ^ 1] = nx;
+            if (nx.valid) {
+                issue_stage(p, nx, bufs0 + static_cast<uint32_t>((buf ^ 1) * buf_bytes), bar0 + 8 * (buf ^ 1),
+                            tables + (buf ^ 1) * kStageTrees);
+            }
+        }
+        const ItemInfo ii = item_info(p, s.item);
+        const int64_t tile0 = static_cast<int64_t>(ii.tile) * TA;
+        const int n_here = static_cast<int>(min(static_cast<int64_t>(TA), p.n_apps - tile0));
+        if (ii.tile != row_tile || ii.model != row_model) {
+            // Stage the tile's ranks transposed: srank[col * TA + app].
+            const int F = p.n_cols;
+            const uint16_t* src = p.ranks + (static_cast<int64_t>(ii.model) * p.n_apps + tile0) * F;
+            for (int i = threadIdx.x; i < n_here * F; i += blockDim.x) {
+                const int app = i / F, col = i - app * F;
+                srank[col * TA + app] = src[i];
+            }
+            __syncthreads();
+            row_tile = ii.tile;
+            row_model = ii.model;
+        }
+        mbar_wait(bar0 + 8 * buf, (phase >> buf) & 1u);
+        phase ^= 1u << buf;
+
+        const int li = group * 32 + lane;
+        const bool valid = li < n_here;
+        WalkCtx c0;  // rank base of the tile (jobs add their own app)
+        c0.wnodes = p.wnodes[ii.model];
+        c0.gnodes = p.gnodes[ii.model];
+        c0.row_saddr = smem_addr(srank);
+        c0.row_stride = TA * 2;
+        WalkCtx c = c0;
+        c.row_saddr += static_cast<uint32_t>((valid ? li : 0) * 2);
+        const int32_t nt = p.n_trees[ii.model];
+        TreeRec* out = p.rec[ii.model];
+        int count = 0;
+        // This warp walks trees 2q + sub of four consecutive pairs side by side.
+        const int4* table = tables + buf * kStageTrees;
+        constexpr int NW = 4;
+        const int32_t t_last = min(2 * s.q1, nt) - 1;
+        for (int32_t q = s.q0; q < s.q1; q += NW) {
+            TreeSrc src[NW];
+            int32_t tt[NW];
+            bool vv[NW];
+            Walk w[NW];
+#pragma unroll
+            for (int h = 0; h < NW; ++h) {
+                tt[h] = 2 * (q + h) + sub;
+                vv[h] = valid && q + h < s.q1 && tt[h] < nt;
+                const int4 e = table[min(tt[h], t_last) - 2 * s.q0];
+                src[h].wroot = e.x;
+                src[h].groot = e.y;
+                src[h].win = kAllSmem ? 0xffffffffu : static_cast<uint32_t>(e.z);
+                src[h].saddr = static_cast<uint32_t>(e.w);
+                w[h] = Walk{0, 0, 0};
+            }
+            walkn<kAllSmem, NW>(c, src, vv, w);
+#pragma unroll
+            for (int h = 0; h < NW; ++h)
+                finish_walk<kAllSmem>(p, c0, c, jobs, count, lane, vv[h], w[h], tt[h], src[h].saddr, li, ii.model,
+                                      out, tile0);
+        }
+        if (count > 0) run_jobs<kAllSmem>(p, c0, jobs, count, lane, ii.model, out, tile0);
+    }
+}
+
+// Ranks of the batch's rows for both models: ranks[m][la][f] = #{thresholds
+// of model m on feature f that are < x} (NaN: their count); the time model
+// sees the time-encoded categorical columns.
+__global__ void grid_rank_kernel(const double* __restrict__ rows, const double* __restrict__ cat_t,
+                                 const int32_t* __restrict__ cat_cols, int32_t n_cat, int64_t a0, int32_t n_apps,
+                                 int32_t F, const double* __restrict__ thr_e, const int32_t* __restrict__ off_e,
+                                 const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
+                                 uint16_t* __restrict__ ranks) {
+    const int64_t total = 2LL * n_apps * F;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int m = static_cast<int>(i / (static_cast<int64_t>(n_apps) * F));
+        const int64_t rem = i - static_cast<int64_t>(m) * n_apps * F;
+        const int64_t la = rem / F;
+        const int f = static_cast<int>(rem - la * F);
+        double x = __ldg(rows + (a0 + la) * F + f);
+        if (m == 1) {
+            for (int k = 0; k < n_cat; ++k)
+                if (__ldg(cat_cols + k) == f) x = __ldg(cat_t + (a0 + la) * n_cat + k);
+        }
+        const double* thr = m ? thr_t : thr_e;
+        const int32_t* off = m ? off_t : off_e;
+        const int32_t o = __ldg(off + f);
+        ranks[i] = static_cast<uint16_t>(rank_of(thr + o, __ldg(off + f + 1) - o, x));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: accumulate + select.
+// ---------------------------------------------------------------------------
+
+// Resident CTAs per SM the accumulate kernel is compiled for (register cap
+// 65536 / (128 * N)).
+#ifndef GD_ACC_MIN_BLOCKS
+#define GD_ACC_MIN_BLOCKS 6
+#endif
+constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
+constexpr int kAccThreads = kAccWarps * 32;
+
+// Per-warp shared region: value ring [3][32] | meta ring [3][32] | right-leaf
+// values [2][32] | residue-table slots [2][kSide] | overflow slot | row.
+constexpr int kSide = 8;
+constexpr int kOffVal = 0;
+constexpr int kOffMeta = kOffVal + 3 * 32 * 8;
+constexpr int kOffRv = kOffMeta + 3 * 32 * 8;
+constexpr int kOffSide = kOffRv + 2 * 32 * 8;
+constexpr int kOffOvf = kOffSide + 2 * kSide * 128;
+constexpr int kOffRow = kOffOvf + 128;
+__host__ __device__ constexpr size_t acc_smem_per_warp(int n_cols) {
+    return static_cast<size_t>(kOffRow) + static_cast<size_t>((n_cols + 1) & ~1) * 8;
+}
+__host__ __device__ constexpr size_t acc_smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+struct AccModel {
     const PNode* nodes;
-    const int32_t* roots;
+    const TreeRec* rec;
     int32_t n_trees;
 };
 
-__device__ __forceinline__ int clamp16(int t) { return min(max(t, 0), 65535); }
-
-// Packed comparison key of a clock test (see the header comment).
-__device__ __forceinline__ int clock_key(bool on_mem, double thr) {
-    const int t = clamp16(thr_to_int(thr));
-    return on_mem ? t : static_cast<int>((static_cast<unsigned>(t) << 16) | 0xffffu);
-}
-
-// AND-mask applied to a packed clock before comparing with the key.
-__device__ __forceinline__ int clock_mask(bool on_mem) { return on_mem ? 0xffff : -1; }
-
-__device__ __forceinline__ bool goes_left(int mask, int key, unsigned ck) {
-    return (ck & static_cast<unsigned>(mask)) <= static_cast<unsigned>(key);
-}
-
-__device__ __forceinline__ int4 residue_node(bool on_mem, double thr) {
-    return make_int4(clock_mask(on_mem), clock_key(on_mem, thr), 0, 0);
-}
-
-
-// One row-only walk state: current node, its value / feature / left child.
-struct Walk {
-    int32_t n, feat, aux;
-    double v;
-};
-
-// Two independent row-only walks advanced side by side (two load chains in
-// flight) until each reaches a leaf or a clock node.  Invalid walks are
-// skipped.
-// Nodes are the grid variant (clock columns recoded negative), so a walk
-// stops at the first node with feat < 0.  Loads are unconditional (a
-// finished or invalid walk re-reads its current node) to keep the loop free
-// of predicated moves.
-__device__ __forceinline__ void walk2(const PNode* __restrict__ nodes, bool va, Walk& a, bool vb, Walk& b,
-                                      const double* row) {
-    load_node(nodes, a.n, a.v, a.feat, a.aux);
-    load_node(nodes, b.n, b.v, b.feat, b.aux);
-    bool ga = va && a.feat >= 0, gb = vb && b.feat >= 0;
-    while (ga || gb) {
-        const double xa = row[ga ? a.feat : 0], xb = row[gb ? b.feat : 0];
-        a.n = ga ? ((xa <= a.v) ? a.aux : a.aux + 1) : a.n;
-        b.n = gb ? ((xb <= b.v) ? b.aux : b.aux + 1) : b.n;
-        load_node(nodes, a.n, a.v, a.feat, a.aux);
-        load_node(nodes, b.n, b.v, b.feat, b.aux);
-        ga = ga && a.feat >= 0;
-        gb = gb && b.feat >= 0;
-    }
-}
-
-// Residue pool allocation state of one warp (warp-uniform).
-struct Alloc {
-    int n_rn, n_rl, tail;
-    unsigned fb_lo, fb_hi;
-};
-
-// Record the end of one queued walk per lane (a group of <= 32 items): a leaf
-// becomes a residue leaf, a clock node a residue node with two new queued
-// walks; the parent's child code is patched.  Ballot-prefix allocation keeps
-// each group's allocations in lane order, so what fits is a prefix.  Items
-// that do not fit mark their tree for fallback.
-__device__ __forceinline__ void place(bool have, int2 item, const Walk& w, int mem_col, const Scratch& s, unsigned lt,
-                                      Alloc& al) {
-    const bool leaf = have && w.feat == kFeatLeaf, node = have && w.feat != kFeatLeaf;
-    const unsigned mleaf = __ballot_sync(kFull, leaf);
-    const unsigned mnode = __ballot_sync(kFull, node);
-    const int tree = item.y >> 16, dest = item.y & 0xffff;
-    const int node_room = min(kRnCap - al.n_rn, (kQCap - al.tail) / 2);  // tail, kQCap even
-    bool over = false;
-    int child = 0;
-    if (leaf) {
-        const int li = al.n_rl + __popc(mleaf & lt);
-        if (li < kRlCap) {
-            s.rl()[li] = w.v;
-            child = ~li;
-        } else {
-            over = true;
-        }
-    }
-    if (node) {
-        const int p = __popc(mnode & lt);
-        const int ri = al.n_rn + p, q2 = al.tail + 2 * p;
-        if (p < node_room) {
-            s.rn()[ri] = residue_node(w.feat == kFeatMem, w.v);
-            s.q()[q2] = make_int2(w.aux, (ri * 2) | (tree << 16));
-            s.q()[q2 + 1] = make_int2(w.aux + 1, (ri * 2 + 1) | (tree << 16));
-            child = ri;
-        } else {
-            over = true;
-        }
-    }
-    if (have && !over) reinterpret_cast<int*>(s.rn())[(dest >> 1) * 4 + 2 + (dest & 1)] = child;
-    al.fb_lo |= __reduce_or_sync(kFull, over && tree < 32 ? (1u << tree) : 0u);
-    al.fb_hi |= __reduce_or_sync(kFull, over && tree >= 32 ? (1u << (tree - 32)) : 0u);
-    al.n_rl += max(0, min(__popc(mleaf), kRlCap - al.n_rl));
-    const int nodes_fit = max(0, min(__popc(mnode), node_room));
-    al.n_rn += nodes_fit;
-    al.tail += 2 * nodes_fit;
-}
-
-// Phase 1 for the chunk [t0, t0 + nt), nt <= 64: fills cval / root / first /
-// rn / rl.  Lane l walks trees l and 32 + l side by side (two independent
-// load chains).  Returns the masks of non-constant trees and of trees whose
-// residue did not fit the pool (those fall back to per-clock traversal from
-// `first`).
-__device__ __forceinline__ void expand_chunk(const ModelRef& m, int32_t t0, int nt, const double* row, int sm_col,
-                                             int mem_col, const Scratch& s, int lane, uint64_t& nonconst,
-                                             uint64_t& fallback) {
-    const unsigned lt = (1u << lane) - 1u;
-    const bool va = lane < nt, vb = lane + 32 < nt;
-    Walk a{0, -1, 0, 0.0}, b{0, -1, 0, 0.0};
-    if (va) a.n = __ldg(m.roots + t0 + lane);
-    if (vb) b.n = __ldg(m.roots + t0 + 32 + lane);
-    walk2(m.nodes, va, a, vb, b, row);
-    const bool ca = va && a.feat != kFeatLeaf, cb = vb && b.feat != kFeatLeaf;
-    if (va && !ca) s.cval()[lane] = a.v;
-    if (vb && !cb) s.cval()[32 + lane] = b.v;
-    const unsigned ma = __ballot_sync(kFull, ca), mb = __ballot_sync(kFull, cb);
-    nonconst = static_cast<uint64_t>(ma) | (static_cast<uint64_t>(mb) << 32);
-    fallback = 0u;
-    if (nonconst == 0u) return;
-    Alloc al;
-    al.n_rn = __popc(ma) + __popc(mb);  // <= 64 <= kRnCap
-    al.tail = 2 * al.n_rn;              // <= 128 <= kQCap
-    al.n_rl = 0;
-    al.fb_lo = al.fb_hi = 0u;
-    if (ca) {
-        const int idx = __popc(ma & lt);
-        s.rn()[idx] = residue_node(a.feat == kFeatMem, a.v);
-        s.root()[lane] = idx;
-        s.first()[lane] = a.n;
-        s.q()[2 * idx] = make_int2(a.aux, (idx * 2) | (lane << 16));
-        s.q()[2 * idx + 1] = make_int2(a.aux + 1, (idx * 2 + 1) | (lane << 16));
-    }
-    if (cb) {
-        const int idx = __popc(ma) + __popc(mb & lt);
-        s.rn()[idx] = residue_node(b.feat == kFeatMem, b.v);
-        s.root()[32 + lane] = idx;
-        s.first()[32 + lane] = b.n;
-        s.q()[2 * idx] = make_int2(b.aux, (idx * 2) | ((32 + lane) << 16));
-        s.q()[2 * idx + 1] = make_int2(b.aux + 1, (idx * 2 + 1) | ((32 + lane) << 16));
-    }
-    __syncwarp();
-    // Breadth-first rounds over the queue, two items per lane per iteration.
-    int head = 0;
-    while (head < al.tail) {
-        const int end = min(head + 64, al.tail);  // items queued before this iteration
-        const int qa = head + lane, qb = head + 32 + lane;
-        const bool ha = qa < end, hb = qb < end;
-        int2 ia = make_int2(0, 0), ib = make_int2(0, 0);
-        if (ha) {
-            ia = s.q()[qa];
-            a.n = ia.x;
-        }
-        if (hb) {
-            ib = s.q()[qb];
-            b.n = ib.x;
-        }
-        walk2(m.nodes, ha, a, hb, b, row);
-        place(ha, ia, a, mem_col, s, lt, al);
-        place(hb, ib, b, mem_col, s, lt, al);
-        head = end;
-        __syncwarp();
-    }
-    fallback = static_cast<uint64_t>(al.fb_lo) | (static_cast<uint64_t>(al.fb_hi) << 32);
-    // Resolve each non-constant tree into a flat record (the queue is dead
-    // now; the key records alias it): lane l handles trees l and 32 + l.
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-        const int t = lane + 32 * half;
-        if (t >= nt || !((nonconst >> t) & 1ull)) continue;
-        unsigned char type;
-        int4 key = make_int4(0, 0, 0, 0);
-        if ((fallback >> t) & 1ull) {
-            type = kFallbackTree;
-            key.x = s.first()[t];
-        } else {
-            const int4 r = s.rn()[s.root()[t]];
-            if (r.z < 0 && r.w < 0) {
-                type = r.x == -1 ? kSingleSm : kSingleMem;
-                s.cval()[t] = s.rl()[~r.z];
-                s.cv2()[t] = s.rl()[~r.w];
-                key = r;
-            } else {
-                const bool node_left = r.z >= 0;
-                const int4 c = s.rn()[node_left ? r.z : r.w];
-                if ((r.z < 0) != (r.w < 0) && c.z < 0 && c.w < 0) {
-                    type = node_left ? kDoubleLeft : kDoubleRight;
-                    s.cval()[t] = s.rl()[~(node_left ? r.w : r.z)];
-                    s.cv2()[t] = s.rl()[~c.z];
-                    s.cv3()[t] = s.rl()[~c.w];
-                    key = make_int4(r.x, r.y, c.x, c.y);
-                } else {
-                    type = kDagTree;
-                    key.x = s.root()[t];
-                }
-            }
-        }
-        s.ttype()[t] = type;
-        s.key()[t] = key;
-    }
-}
-
-// Full per-candidate traversal from node n (grid-variant nodes) with a packed
-// clock: predict_row on the substituted row (models.cpp:71-78).
+// Full per-candidate traversal from node n (grid nodes) with a packed clock:
+// predict_row on the substituted row (models.cpp:71-78).
 __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nodes, int32_t n, const double* row,
                                                    unsigned ck) {
     const double sm = static_cast<double>(ck >> 16), mem = static_cast<double>(ck & 0xffffu);
@@ -333,107 +680,191 @@ __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nod
     }
 }
 
-template <int CPL>
-__device__ __forceinline__ void accumulate_model(const ModelRef& m, const double* row, int sm_col, int mem_col,
-                                                 const Scratch& s, const unsigned (&ck)[CPL], int lane,
-                                                 double (&acc)[CPL]) {
-    for (int32_t t0 = 0; t0 < m.n_trees; t0 += kChunk) {
-        const int nt = min(kChunk, m.n_trees - t0);
-        uint64_t nonconst, fallback;
-        expand_chunk(m, t0, nt, row, sm_col, mem_col, s, lane, nonconst, fallback);
-        __syncwarp();
-        for (int h = 0; h < kChunk; h += 32) {
-            const int nth = min(32, nt - h);
-            if (nth <= 0) break;
-            const unsigned nc = static_cast<unsigned>(nonconst >> h);
-            int jj = 0;
-            while (jj < nth) {
-                // A run of constant trees jj .. jj+run-1, then one non-constant tree.
-                const unsigned rest = nc >> jj;
-                const int run = rest ? min(__ffs(rest) - 1, nth - jj) : nth - jj;
-                const double* cv = s.cval() + h + jj;
-                int k = 0;
-                for (; k + 3 < run; k += 4) {
-                    const double v0 = cv[k], v1 = cv[k + 1], v2 = cv[k + 2], v3 = cv[k + 3];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v1);
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v2);
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v3);
-                }
-                for (; k < run; ++k) {
-                    const double v0 = cv[k];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v0);
-                }
-                jj += run;
-                if (jj >= nth) break;
-                const int j = h + jj;
-                ++jj;
-                const unsigned char type = s.ttype()[j];
-                const int4 kk = s.key()[j];
-                const unsigned rmask = static_cast<unsigned>(kk.x), rkey = static_cast<unsigned>(kk.y);
-                if (type == kSingleSm) {
-                    // One clock test between two leaves: compare + select.
-                    const double lv = s.cval()[j], rv = s.cv2()[j];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= rkey ? lv : rv);
-                } else if (type == kSingleMem) {
-                    const double lv = s.cval()[j], rv = s.cv2()[j];
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= rkey ? lv : rv);
-                } else if (type == kDoubleLeft || type == kDoubleRight) {
-                    // Two tests: the root and one child test, three leaves.
-                    const double solo = s.cval()[j], cl = s.cv2()[j], cr = s.cv3()[j];
-                    const unsigned cmask = static_cast<unsigned>(kk.z), ckey = static_cast<unsigned>(kk.w);
-                    if (type == kDoubleLeft) {
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) {
-                            const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
-                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= rkey ? sub : solo);
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < CPL; ++i) {
-                            const double sub = (ck[i] & cmask) <= ckey ? cl : cr;
-                            acc[i] = __dadd_rn(acc[i], (ck[i] & rmask) <= rkey ? solo : sub);
-                        }
-                    }
-                } else if (type == kDagTree) {
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) {
-                        int code = kk.x;
-                        while (code >= 0) {
-                            const int4 q = s.rn()[code];
-                            code = goes_left(q.x, q.y, ck[i]) ? q.z : q.w;
-                        }
-                        acc[i] = __dadd_rn(acc[i], s.rl()[~code]);
-                    }
-                } else {  // kFallbackTree
-#pragma unroll
-                    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, kk.x, row, ck[i]));
-                }
-            }
-        }
-        __syncwarp();
+// Stage 1 of the ring: the value and meta words of tree g*32 + lane.
+__device__ __forceinline__ void issue_rec(const AccModel& m, int64_t la, int64_t n_apps, int g, int lane,
+                                          uint32_t ws) {
+    const int32_t t = g * 32 + lane;
+    if (t < m.n_trees) {
+        const TreeRec* src = m.rec + rec_index(t, la, n_apps);
+        const uint32_t slot = static_cast<uint32_t>(((g % 3) * 32 + lane) * 8);
+        cp_async8(ws + kOffVal + slot, &src->v);
+        cp_async8(ws + kOffMeta + slot, &src->info);
     }
 }
 
-// Named barrier for one warp pair.  The warp reconverges first (independent
-// thread scheduling does not guarantee it after the data-dependent loops),
-// and the non-.aligned form is used.
-// Barrier ids are immediates: a register id makes ptxas reserve all 16
-// named barriers per CTA, which caps residency at 4 CTAs per SM.
+// Stage 2: the side data the record points at (right leaf value / residue
+// table).  Returns the group's residue-table mask (slot = rank in it).
+__device__ __forceinline__ unsigned issue_side(const AccModel& m, const RTRec* __restrict__ pool, int g, int lane,
+                                               uint32_t ws) {
+    const int32_t t = g * 32 + lane;
+    uint2 meta = make_uint2(kRecConst, 0u);
+    if (t < m.n_trees) meta = lds_u2(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 8));
+    const uint32_t kind = meta.x & 7u;
+    const unsigned tm = __ballot_sync(kFull, kind == kRecTable);
+    if (kind == kRecSm || kind == kRecMem) {
+        cp_async8(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + lane) * 8), &m.nodes[static_cast<int32_t>(meta.y)].v);
+    } else if (kind == kRecTable) {
+        const int slot = __popc(tm & ((1u << lane) - 1u));
+        if (slot < kSide) {
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(pool + meta.y);
+            const uint32_t dst = ws + kOffSide + static_cast<uint32_t>(((g & 1) * kSide + slot) * 128);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cp_async16(dst + 16 * k, src + 16 * k);
+        }
+    }
+    return tm;
+}
+
+template <int CPL>
+__device__ __forceinline__ void add_const(double (&acc)[CPL], double v) {
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], v);
+}
+
+// Residue table at shared address sb, depth D (2 or 3).
+template <int CPL, int D>
+__device__ __forceinline__ void add_table(double (&acc)[CPL], const unsigned (&ck)[CPL], uint32_t sb) {
+    const uint2 t0 = lds_u2(sb);
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+        uint32_t n = 1u + ((ck[i] & t0.x) > t0.y ? 1u : 0u);
+#pragma unroll
+        for (int d = 1; d < D; ++d) {
+            const uint2 t = lds_u2(sb + n * 8u);
+            n = 2u * n + 1u + ((ck[i] & t.x) > t.y ? 1u : 0u);
+        }
+        acc[i] = __dadd_rn(acc[i], lds_f64(sb + 64u + (n - ((1u << D) - 1u)) * 8u));
+    }
+}
+
+// The group's per-kind tree masks (ballots: warp-uniform, so the per-tree
+// dispatch below is uniform branching).
+struct GroupMasks {
+    unsigned nc, sm, mem, tab;
+};
+
+// One non-constant tree j of the group being processed.
+template <int CPL>
+__device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __restrict__ pool, uint32_t ws, int g,
+                                            int j, const GroupMasks& gm, const double* row,
+                                            const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l, int lane,
+                                            double (&acc)[CPL]) {
+    const uint32_t slotb = static_cast<uint32_t>(((g % 3) * 32 + j) * 8);
+    const unsigned bit = 1u << j;
+    if (gm.sm & bit) {
+        const uint32_t info = lds_u32(ws + kOffMeta + slotb);
+        const double lv = lds_f64(ws + kOffVal + slotb);
+        const double rv = lds_f64(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + j) * 8));
+        const unsigned key = (info & 0xffff0000u) | 0xffffu;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= key ? lv : rv);
+    } else if (gm.mem & bit) {
+        const uint32_t info = lds_u32(ws + kOffMeta + slotb);
+        const double lv = lds_f64(ws + kOffVal + slotb);
+        const double rv = lds_f64(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + j) * 8));
+        const unsigned key = info >> 16;
+        if (mem_uniform) {  // all of this lane's clocks share one memory clock
+            add_const<CPL>(acc, mem_l <= key ? lv : rv);
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & 0xffffu) <= key ? lv : rv);
+        }
+    } else if (gm.tab & bit) {
+        const int slot = __popc(gm.tab & (bit - 1u));
+        uint32_t sb;
+        if (slot < kSide) {
+            sb = ws + kOffSide + static_cast<uint32_t>(((g & 1) * kSide + slot) * 128);
+        } else {  // more tables in this group than staged slots: copy it now
+            const uint32_t ref = lds_u32(ws + kOffMeta + slotb + 4);
+            sb = ws + kOffOvf;
+            __syncwarp();
+            if (lane < 8) {
+                const int4 x = __ldg(reinterpret_cast<const int4*>(pool + ref) + lane);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * lane), "r"(x.x), "r"(x.y),
+                             "r"(x.z), "r"(x.w)
+                             : "memory");
+            }
+            __syncwarp();
+        }
+        if (lds_u32(sb + 56u) == 2u) add_table<CPL, 2>(acc, ck, sb);
+        else add_table<CPL, 3>(acc, ck, sb);
+    } else {
+        const int32_t ref = static_cast<int32_t>(lds_u32(ws + kOffMeta + slotb + 4));
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, ref, row, ck[i]));
+    }
+}
+
+template <int CPL>
+__device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec* __restrict__ pool, int64_t la,
+                                                 int64_t n_apps, const double* row, uint32_t ws,
+                                                 const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l,
+                                                 int lane, double (&acc)[CPL]) {
+    const int ng = (m.n_trees + 31) >> 5;
+    if (ng == 0) return;
+    __syncwarp();
+    issue_rec(m, la, n_apps, 0, lane, ws);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    issue_side(m, pool, 0, lane, ws);
+    if (ng > 1) issue_rec(m, la, n_apps, 1, lane, ws);
+    cp_async_commit();
+    for (int g = 0; g < ng; ++g) {
+        cp_async_wait_all();
+        __syncwarp();
+        if (g + 1 < ng) issue_side(m, pool, g + 1, lane, ws);
+        if (g + 2 < ng) issue_rec(m, la, n_apps, g + 2, lane, ws);
+        cp_async_commit();
+
+        const int nth = min(32, m.n_trees - g * 32);
+        const uint32_t vals = ws + kOffVal + static_cast<uint32_t>((g % 3) * 32 * 8);
+        const uint32_t kind_l = lane < nth ? (lds_u32(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 8)) & 7u)
+                                           : kRecConst;
+        GroupMasks gm;
+        gm.nc = __ballot_sync(kFull, kind_l != kRecConst);
+        gm.sm = __ballot_sync(kFull, kind_l == kRecSm);
+        gm.mem = __ballot_sync(kFull, kind_l == kRecMem);
+        gm.tab = __ballot_sync(kFull, kind_l == kRecTable);
+        // Runs of constant trees between residue trees (uniform control flow).
+        unsigned rest = gm.nc;
+        int j = 0;
+        while (true) {
+            const int r = rest ? __ffs(rest) - 1 : nth;
+            int k = j;
+            for (; k + 4 <= r; k += 4) {
+                const double v0 = lds_f64(vals + static_cast<uint32_t>(k * 8));
+                const double v1 = lds_f64(vals + static_cast<uint32_t>(k * 8 + 8));
+                const double v2 = lds_f64(vals + static_cast<uint32_t>(k * 8 + 16));
+                const double v3 = lds_f64(vals + static_cast<uint32_t>(k * 8 + 24));
+                add_const<CPL>(acc, v0);
+                add_const<CPL>(acc, v1);
+                add_const<CPL>(acc, v2);
+                add_const<CPL>(acc, v3);
+            }
+            if (k + 2 <= r) {
+                const double v0 = lds_f64(vals + static_cast<uint32_t>(k * 8));
+                const double v1 = lds_f64(vals + static_cast<uint32_t>(k * 8 + 8));
+                add_const<CPL>(acc, v0);
+                add_const<CPL>(acc, v1);
+                k += 2;
+            }
+            if (k < r) add_const<CPL>(acc, lds_f64(vals + static_cast<uint32_t>(k * 8)));
+            if (r >= nth) break;
+            add_residue<CPL>(m, pool, ws, g, r, gm, row, ck, mem_uniform, mem_l, lane, acc);
+            rest &= rest - 1u;
+            j = r + 1;
+        }
+    }
+}
+
+// Named barrier for one warp pair (ids are immediates: a register id makes
+// ptxas reserve all 16 named barriers per CTA).
 template <int kId>
 __device__ __forceinline__ void pair_sync() {
     __syncwarp();
     asm volatile("barrier.sync %0, 64;" ::"n"(kId) : "memory");
 }
-
-// Barrier A (pair 0: id 1, pair 1: id 3) and barrier B (ids 2 / 4).
 __device__ __forceinline__ void pair_sync_a(int pair) {
     if (pair == 0) pair_sync<1>();
     else pair_sync<3>();
@@ -443,60 +874,149 @@ __device__ __forceinline__ void pair_sync_b(int pair) {
     else pair_sync<4>();
 }
 
+// The catalog -> (lane, slot) map, built by one warp into map[slot * 32 +
+// lane] (catalog index or -1).  Preferred: every lane's clocks lie in ONE run
+// of equal memory clocks (catalog order groups them: mem asc, sm asc), so a
+// memory-clock test is one compare per lane; runs take consecutive lanes,
+// slots in catalog order, so lane-major slot order is still catalog order.
+// If the runs need more than 32 lanes, lane l owns clocks l*cpl .. l*cpl+cpl-1.
+// Returns 1 for the per-lane-uniform memory clock layout.
+__device__ int build_clock_map(const int32_t* __restrict__ mem, int C, int cpl, int16_t* map, int lane) {
+    constexpr int K = 16;  // clocks per lane (C <= 512)
+    for (int i = 0; i < cpl; ++i) map[i * 32 + lane] = -1;
+    const int c0 = lane * K;
+    // Run starts in my chunk.
+    unsigned starts = 0;
+    int prev = c0 > 0 && c0 < C ? __ldg(mem + c0 - 1) : 0;
+    for (int k = 0; k < K; ++k) {
+        const int c = c0 + k;
+        if (c >= C) break;
+        const int mv = __ldg(mem + c);
+        if (c == 0 || mv != prev) starts |= 1u << k;
+        prev = mv;
+    }
+    // Last start at or before my chunk (max-scan) and first start after it (min-scan).
+    int last_in = starts ? c0 + 31 - __clz(static_cast<int>(starts)) : -1;
+    int first_in = starts ? c0 + __ffs(starts) - 1 : C;
+    int carry_last = last_in, carry_first = first_in;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(kFull, carry_last, d);
+        const int b = __shfl_down_sync(kFull, carry_first, d);
+        if (lane >= d) carry_last = max(carry_last, a);
+        if (lane + d < 32) carry_first = min(carry_first, b);
+    }
+    int before_last = __shfl_up_sync(kFull, carry_last, 1);    // last start before my chunk
+    int after_first = __shfl_down_sync(kFull, carry_first, 1);  // first start after my chunk
+    if (lane == 0) before_last = -1;
+    if (lane == 31) after_first = C;
+    // Lanes used by the runs that START in my chunk, then an exclusive scan.
+    int mine = 0;
+    for (int k = 0; k < K; ++k) {
+        if (!((starts >> k) & 1u)) continue;
+        const unsigned later = starts & ~((2u << k) - 1u);
+        const int end = later ? c0 + __ffs(later) - 1 : after_first;
+        mine += (end - (c0 + k) + cpl - 1) / cpl;
+    }
+    int incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int a = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += a;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int uniform = total <= 32;
+    __syncwarp();
+    // Base lane of the run in progress at c0 (it started before my chunk).
+    int run_start = before_last, base = incl - mine;
+    if (run_start >= 0) {
+        const int end = starts ? c0 + __ffs(starts) - 1 : after_first;
+        base -= (end - run_start + cpl - 1) / cpl;
+    }
+    for (int k = 0; k < K; ++k) {
+        const int c = c0 + k;
+        if (c >= C) break;
+        if ((starts >> k) & 1u) {
+            if (run_start >= 0 && run_start >= c0) {
+                // previous run started in my chunk: advance the base past it
+                base += (c - run_start + cpl - 1) / cpl;
+            } else if (run_start >= 0) {
+                base += (c - run_start + cpl - 1) / cpl;
+            }
+            run_start = c;
+        }
+        if (uniform) {
+            const int off = c - run_start;
+            map[(off % cpl) * 32 + base + off / cpl] = static_cast<int16_t>(c);
+        } else {
+            map[(c % cpl) * 32 + c / cpl] = static_cast<int16_t>(c);
+        }
+    }
+    __syncwarp();
+    return uniform;
+}
+
 template <int CPL>
-__global__ void __launch_bounds__(kThreads, (CPL >= 12 ? 4 : GD_GRID_MIN_BLOCKS))
-    grid_partial_kernel(const __grid_constant__ GridParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCKS)) grid_acc_kernel(const __grid_constant__ AccParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
-    const bool is_time = warp & 1;
+    const int model = warp & 1;  // 0 energy, 1 time
     const int F = p.n_cols;
-    Scratch s;
-    s.base = smem + smem_per_warp(F) * warp;
-    double* const row = s.row();
-    double* tbuf = reinterpret_cast<double*>(smem + smem_per_warp(F) * kWarps + smem_per_pair(CPL) * pair);
+    unsigned char* wsp = smem + acc_smem_per_warp(F) * warp;
+    const uint32_t ws = smem_addr(wsp);
+    double* row = reinterpret_cast<double*>(wsp + kOffRow);
+    double* tbuf = reinterpret_cast<double*>(smem + acc_smem_per_warp(F) * kAccWarps + acc_smem_per_pair(CPL) * pair);
+    int16_t* map = reinterpret_cast<int16_t*>(smem + acc_smem_per_warp(F) * kAccWarps +
+                                              acc_smem_per_pair(CPL) * (kAccWarps / 2));
+    int* flag = reinterpret_cast<int*>(map + 32 * CPL);
+    if (warp == 0) {
+        const int u = build_clock_map(p.mem, p.n_clocks, CPL, map, lane);
+        if (lane == 0) *flag = u;
+    }
+    __syncthreads();
+    const bool mem_uniform = *flag != 0;
 
     unsigned ck[CPL];
+    unsigned mem_l = 0;
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
-        const int c = lane * CPL + i;  // lane l owns clocks l*CPL .. l*CPL+CPL-1
-        ck[i] = c < p.n_clocks ? ((static_cast<unsigned>(__ldg(p.sm + c)) << 16) | static_cast<unsigned>(__ldg(p.mem + c)))
-                               : 0u;
+        const int c = map[i * 32 + lane];
+        ck[i] = c >= 0 ? ((static_cast<unsigned>(__ldg(p.sm + c)) << 16) | static_cast<unsigned>(__ldg(p.mem + c))) : 0u;
+        if (i == 0) mem_l = ck[0] & 0xffffu;
     }
-    // Field-wise selects (a ternary over two ModelRef aggregates built from
-    // __grid_constant__ fields picked the energy model for both roles).
-    ModelRef m;
-    m.nodes = is_time ? p.t_nodes : p.e_nodes;
-    m.roots = is_time ? p.t_roots : p.e_roots;
-    m.n_trees = is_time ? p.t_trees : p.e_trees;
-    const int sm_col = p.sm_col, mem_col = p.mem_col;
+    AccModel m;
+    m.nodes = model ? p.nodes[1] : p.nodes[0];
+    m.rec = model ? p.rec[1] : p.rec[0];
+    m.n_trees = model ? p.n_trees[1] : p.n_trees[0];
 
-    for (int64_t a = static_cast<int64_t>(blockIdx.x) * (kWarps / 2) + pair; a < p.n_apps;
-         a += static_cast<int64_t>(gridDim.x) * (kWarps / 2)) {
+    for (int64_t la = static_cast<int64_t>(blockIdx.x) * (kAccWarps / 2) + pair; la < p.n_apps;
+         la += static_cast<int64_t>(gridDim.x) * (kAccWarps / 2)) {
+        const int64_t a = p.a0 + la;
         double acc[CPL];
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+        // The row is only read by FULL records (rare); staging it is cheap.
         __syncwarp();
         const double* src = p.rows + a * F;
         for (int j = lane; j < F; j += 32) row[j] = __ldg(src + j);
         __syncwarp();
-        if (is_time) {
-            // the time model sees the time-encoded categorical columns
+        if (model == 1) {
             for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
         }
-        accumulate_model<CPL>(m, row, sm_col, mem_col, s, ck, lane, acc);
-        if (is_time) {
+        accumulate_model<CPL>(m, p.pool, la, p.n_apps, row, ws, ck, mem_uniform, mem_l, lane, acc);
+        if (model == 1) {
             pair_sync_a(pair);  // the energy warp is done reading the previous app's times
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) tbuf[lane * CPL + i] = finish(p.t_base, p.t_lr, acc[i]);
+            for (int i = 0; i < CPL; ++i) tbuf[lane * CPL + i] = finish(p.base[1], p.lr[1], acc[i]);
             pair_sync_b(pair);
         } else {
             double E[CPL], T[CPL];
-            int smv[CPL];
+            int smv[CPL], cidx[CPL];
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
-                E[i] = clamp_energy(finish(p.e_base, p.e_lr, acc[i]));
+                E[i] = clamp_energy(finish(p.base[0], p.lr[0], acc[i]));
                 smv[i] = static_cast<int>(ck[i] >> 16);
             }
             pair_sync_a(pair);
@@ -504,20 +1024,23 @@ __global__ void __launch_bounds__(kThreads, (CPL >= 12 ? 4 : GD_GRID_MIN_BLOCKS)
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
                 T[i] = tbuf[lane * CPL + i];
-                const int c = lane * CPL + i;
-                if (c < p.n_clocks) {
+                const int c = map[i * 32 + lane];
+                cidx[i] = c;
+                if (c >= 0) {
                     if (p.e_out) p.e_out[a * p.n_clocks + c] = E[i];
                     if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
                 }
             }
-            select_epilogue<CPL>(E, T, smv, lane, p.n_clocks, __ldg(p.budgets + a), p.mode, p.objective,
-                                 p.best_effort, p.out + a);
+            select_epilogue<CPL>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective, p.best_effort,
+                                 p.out + a);
         }
     }
 }
 
+// ---------------------------------------------------------------------------
 // Rows genuinely differ per clock (nearest-record substitution from several
 // profiled records, scheduler.cpp:341-359): full traversal per candidate.
+// ---------------------------------------------------------------------------
 template <int CPL>
 __global__ void __launch_bounds__(256) grid_general_kernel(const __grid_constant__ GridParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -566,55 +1089,224 @@ __global__ void __launch_bounds__(256) grid_general_kernel(const __grid_constant
                 if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
             }
         }
-        select_epilogue<CPL>(E, T, smv, lane, p.n_clocks, __ldg(p.budgets + a), p.mode, p.objective,
-                             p.best_effort, p.out + a);
+        int cidx[CPL];
+        contiguous_cidx<CPL>(lane, p.n_clocks, cidx);
+        select_epilogue<CPL>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective, p.best_effort,
+                             p.out + a);
     }
 }
 
 template <int CPL>
-int launch_cpl(const GridParams& p, bool general, int sm_count, cudaStream_t stream) {
-    if (general) {
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_general_kernel<CPL>, 256, 0);
-        const int blocks = grid_blocks(8, p.n_apps, sm_count, per_sm);
-        grid_general_kernel<CPL><<<blocks, 256, 0, stream>>>(p);
-        return cudaGetLastError();
-    }
-    const size_t smem = smem_per_warp(p.n_cols) * kWarps + smem_per_pair(CPL) * (kWarps / 2);
-    auto kern = grid_partial_kernel<CPL>;
+int launch_general(const GridParams& p, int sm_count, cudaStream_t stream) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_general_kernel<CPL>, 256, 0);
+    const int blocks = grid_blocks(8, p.n_apps, sm_count, per_sm);
+    grid_general_kernel<CPL><<<blocks, 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+
+template <int CPL>
+int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
+    const size_t smem = acc_smem_per_warp(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
+                        32 * CPL * sizeof(int16_t) + 16;
+    auto kern = grid_acc_kernel<CPL>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    // Shared-memory carveout (percent of the unified L1/shared array).  The
-    // row-only walks read tree nodes through L1, so L1 capacity beats the
-    // last resident CTAs: measured on B200 (configs[1]) 80% -> 1.04 ms vs
-    // 100% -> 1.17 ms (all-constant trees: 0.40 vs 0.67 ms).
-    // GDVFS_CARVEOUT=<0..100> overrides (experiments).
-    static const int carveout = [] {
-        const char* e = std::getenv("GDVFS_CARVEOUT");
-        return e ? std::atoi(e) : 80;
-    }();
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
-    const int blocks = grid_blocks(kWarps / 2, p.n_apps, sm_count, per_sm);
-    kern<<<blocks, kThreads, smem, stream>>>(p);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAccThreads, smem);
+    const int blocks = grid_blocks(kAccWarps / 2, p.n_apps, sm_count, per_sm);
+    kern<<<blocks, kAccThreads, smem, stream>>>(p);
     return cudaGetLastError();
+}
+
+int launch_acc_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
+    const int cpl = (p.n_clocks + 31) / 32;
+    if (cpl <= 1) return launch_acc<1>(p, sm_count, s);
+    if (cpl <= 2) return launch_acc<2>(p, sm_count, s);
+    if (cpl <= 4) return launch_acc<4>(p, sm_count, s);
+    if (cpl <= 7) return launch_acc<7>(p, sm_count, s);
+    if (cpl <= 9) return launch_acc<9>(p, sm_count, s);
+    if (cpl <= 12) return launch_acc<12>(p, sm_count, s);
+    return launch_acc<16>(p, sm_count, s);
+}
+
+// Walk-kernel geometry: warps per CTA (two per 32 apps) so the transposed
+// ranks plus two stage buffers of tree windows fit the opt-in shared memory.
+struct WalkGeom {
+    int warps, win_nodes, stage_nodes;
+    size_t smem;
+};
+int64_t env_i64(const char* name, int64_t dflt);
+WalkGeom walk_geom(const GridParams& p) {
+    constexpr size_t kLimit = 227 * 1024;
+    WalkGeom g{};
+    g.win_nodes = static_cast<int>(env_i64("GDVFS_WIN_NODES", 512)) & ~1;
+    if (g.win_nodes < 2) g.win_nodes = 2;
+    const int32_t max_pair = (p.e_max_pair_nodes > p.t_max_pair_nodes ? p.e_max_pair_nodes : p.t_max_pair_nodes) + 2;
+    const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
+    for (int groups = 8; groups >= 1; groups >>= 1) {
+        const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(2 * groups) +
+                             2 * kStageTrees * 16;
+        if (fixed + 2 * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
+        g.warps = 2 * groups;
+        int64_t stage = static_cast<int64_t>((kLimit - fixed) / 16) & ~1;
+        if (stage > 16384) stage = 16384;
+        g.stage_nodes = static_cast<int>(stage);
+        g.smem = fixed + 2 * static_cast<size_t>(g.stage_nodes) * 8;
+        return g;
+    }
+    g.warps = 0;  // too many columns
+    return g;
+}
+
+int64_t env_i64(const char* name, int64_t dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoll(e) : dflt;
+}
+
+// Apps per batch: the walk records of one batch stay bounded (and, at the
+// default budget, mostly L2-resident between the two kernels).
+int64_t batch_apps(const GridParams& p) {
+    const int64_t per_app = grid_scratch_per_app(p);
+    static const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 31);
+    int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
+    b = b < 256 ? 256 : b;
+    return b < p.n_apps ? b : p.n_apps;
 }
 
 }  // namespace
 
-int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream) {
+int64_t grid_scratch_per_app(const GridParams& p) {
+    const int64_t pairs = ((p.e_trees + 1) >> 1) + ((p.t_trees + 1) >> 1);
+    const int64_t pool = (static_cast<int64_t>(p.e_trees) + p.t_trees) / 8 + 1;  // residue tables per app
+    const int64_t ranks = (2LL * p.n_cols * 2 + 15) & ~15LL;
+    return pairs * 2 * static_cast<int64_t>(sizeof(TreeRec)) + pool * static_cast<int64_t>(sizeof(RTRec)) + ranks;
+}
+
+size_t grid_scratch_bytes(const GridParams& p, bool general) {
+    if (general || p.n_apps == 0) return 0;
+    const int64_t b = batch_apps(p);
+    const int64_t nb = (p.n_apps + b - 1) / b;
+    return static_cast<size_t>(b * grid_scratch_per_app(p)) + static_cast<size_t>(nb) * 4 + 256;
+}
+
+int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
+                       size_t scratch_bytes, int64_t* launches) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int cpl = (p.n_clocks + 31) / 32;
-    if (cpl <= 1) return launch_cpl<1>(p, general, sm_count, s);
-    if (cpl <= 2) return launch_cpl<2>(p, general, sm_count, s);
-    if (cpl <= 4) return launch_cpl<4>(p, general, sm_count, s);
-    if (cpl <= 7) return launch_cpl<7>(p, general, sm_count, s);
-    if (cpl <= 9) return launch_cpl<9>(p, general, sm_count, s);
-    if (cpl <= 12) return launch_cpl<12>(p, general, sm_count, s);
-    return launch_cpl<16>(p, general, sm_count, s);
+    if (general) {
+        const int cpl = (p.n_clocks + 31) / 32;
+        int e;
+        if (cpl <= 1) e = launch_general<1>(p, sm_count, s);
+        else if (cpl <= 2) e = launch_general<2>(p, sm_count, s);
+        else if (cpl <= 4) e = launch_general<4>(p, sm_count, s);
+        else if (cpl <= 7) e = launch_general<7>(p, sm_count, s);
+        else if (cpl <= 9) e = launch_general<9>(p, sm_count, s);
+        else if (cpl <= 12) e = launch_general<12>(p, sm_count, s);
+        else e = launch_general<16>(p, sm_count, s);
+        if (launches) ++*launches;
+        return e;
+    }
+    if (p.n_apps == 0) return cudaSuccess;
+    if (scratch_bytes < grid_scratch_bytes(p, false)) return cudaErrorInvalidValue;
+    const int64_t B = batch_apps(p);
+    const int64_t nb = (p.n_apps + B - 1) / B;
+    const int64_t pe = (p.e_trees + 1) >> 1, pt = (p.t_trees + 1) >> 1;
+    const int64_t pool_cap = B * ((static_cast<int64_t>(p.e_trees) + p.t_trees) / 8 + 1);
+    unsigned char* base = static_cast<unsigned char*>(scratch);
+    TreeRec* rec_e = reinterpret_cast<TreeRec*>(base);
+    TreeRec* rec_t = rec_e + B * pe * 2;
+    RTRec* pool = reinterpret_cast<RTRec*>(rec_t + B * pt * 2);
+    uint16_t* ranks = reinterpret_cast<uint16_t*>(pool + pool_cap);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(ranks + ((2LL * B * p.n_cols + 7) & ~7LL));
+    cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
+    if (e != cudaSuccess) return e;
+
+    const WalkGeom wg = walk_geom(p);
+    // 16-bit ranks and tree-local child indices bound what the walk handles.
+    if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
+    const bool all_smem = ((p.max_tree_nodes + 1) & ~1) <= wg.win_nodes;
+    auto walk_kern = all_smem ? grid_walk_kernel<true> : grid_walk_kernel<false>;
+    e = cudaFuncSetAttribute(walk_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg.smem));
+    if (e != cudaSuccess) return e;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t a0 = b * B;
+        const int32_t n = static_cast<int32_t>(p.n_apps - a0 < B ? p.n_apps - a0 : B);
+        {
+            const int64_t total = 2LL * n * p.n_cols;
+            int blocks = static_cast<int>((total + 255) / 256);
+            if (blocks > 16 * sm_count) blocks = 16 * sm_count;
+            grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, p.e_thr,
+                                                    p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        WalkParams w{};
+        w.wnodes[0] = p.e_wnodes;
+        w.wnodes[1] = p.t_wnodes;
+        w.wroots[0] = p.e_wroots;
+        w.wroots[1] = p.t_wroots;
+        w.roots[0] = p.e_roots;
+        w.roots[1] = p.t_roots;
+        w.gnodes[0] = p.e_nodes;
+        w.gnodes[1] = p.t_nodes;
+        w.n_trees[0] = p.e_trees;
+        w.n_trees[1] = p.t_trees;
+        w.ranks = ranks;
+        w.n_apps = n;
+        w.n_cols = p.n_cols;
+        w.tile_apps = wg.warps * 16;
+        w.win_nodes = wg.win_nodes;
+        w.stage_nodes = wg.stage_nodes;
+        w.rec[0] = rec_e;
+        w.rec[1] = rec_t;
+        w.pool = pool;
+        w.pool_count = counts + b;
+        w.pool_cap = static_cast<uint32_t>(pool_cap);
+        const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;
+        const int64_t max_pairs = pe > pt ? pe : pt;
+        int64_t splits = (8LL * sm_count + 2 * tiles - 1) / (2 * tiles);
+        if (splits > max_pairs) splits = max_pairs;
+        if (splits < 1) splits = 1;
+        w.splits = static_cast<int32_t>(splits);
+        w.n_items = static_cast<int32_t>(tiles * 2 * splits);
+        const int grid = w.n_items < sm_count ? w.n_items : sm_count;
+        walk_kern<<<grid, wg.warps * 32, wg.smem, s>>>(w);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+        AccParams a{};
+        a.nodes[0] = p.e_nodes;
+        a.nodes[1] = p.t_nodes;
+        a.n_trees[0] = p.e_trees;
+        a.n_trees[1] = p.t_trees;
+        a.base[0] = p.e_base;
+        a.base[1] = p.t_base;
+        a.lr[0] = p.e_lr;
+        a.lr[1] = p.t_lr;
+        a.rec[0] = rec_e;
+        a.rec[1] = rec_t;
+        a.pool = pool;
+        a.rows = p.rows;
+        a.cat_t = p.cat_t;
+        a.cat_cols = p.cat_cols;
+        a.sm = p.sm;
+        a.mem = p.mem;
+        a.budgets = p.budgets;
+        a.out = p.out;
+        a.e_out = p.e_out;
+        a.t_out = p.t_out;
+        a.a0 = a0;
+        a.n_apps = n;
+        a.n_cols = p.n_cols;
+        a.n_cat = p.n_cat;
+        a.n_clocks = p.n_clocks;
+        a.mode = p.mode;
+        a.objective = p.objective;
+        a.best_effort = p.best_effort;
+        if ((e = static_cast<cudaError_t>(launch_acc_cpl(a, sm_count, s))) != cudaSuccess) return e;
+        if (launches) *launches += 3;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace gd

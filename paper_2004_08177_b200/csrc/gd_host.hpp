@@ -37,9 +37,20 @@ struct gd_model {
     int32_t* d_roots = nullptr;
     double* d_coef = nullptr;
     int64_t packed_nodes = 0;
+    int32_t max_pair_nodes = 0;
+    int32_t max_tree_nodes = 0;  // largest packed size of two consecutive trees (2q, 2q+1)
     // Grid variant of d_nodes: the sm / mem clock columns recoded as
     // feat = kFeatSm / kFeatMem (built on first use per column pair).
     mutable gd::PNode* d_grid_nodes = nullptr;
+    // Rank form for the walk kernel: sorted distinct thresholds per feature,
+    // walk-node tree offsets (trees padded to an even count) and the walk
+    // nodes themselves (built with the grid nodes).
+    double* d_thr = nullptr;
+    int32_t* d_thr_off = nullptr;
+    int32_t* d_wroots = nullptr;
+    int64_t n_wnodes = 0;
+    int32_t max_thr_per_feature = 0;
+    mutable gd::WNode* d_wnodes = nullptr;
     mutable int32_t grid_sm_col = -1, grid_mem_col = -1;
 
     int32_t n_trees() const { return offsets.empty() ? 0 : static_cast<int32_t>(offsets.size() - 1); }

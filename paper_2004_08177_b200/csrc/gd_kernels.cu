@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ Sel
             E[i] = c < p.n_clocks ? __ldg(p.energy + a * p.n_clocks + c) : 0.0;
             T[i] = c < p.n_clocks ? __ldg(p.time + a * p.n_clocks + c) : 0.0;
         }
-        select_epilogue<CPL>(E, T, smv, lane, p.n_clocks, __ldg(p.budgets + a), p.mode, p.objective,
-                             p.best_effort, p.out + a);
+        int cidx[CPL];
+        contiguous_cidx<CPL>(lane, p.n_clocks, cidx);
+        select_epilogue<CPL>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective, p.best_effort,
+                             p.out + a);
     }
 }
 
@@ -144,6 +146,41 @@ __global__ void recode_clock_nodes_kernel(const PNode* __restrict__ src, PNode* 
             else if (x.feat == mem_col) x.feat = kFeatMem;
         }
         dst[i] = x;
+    }
+}
+
+// Walk nodes (gd_device.cuh WNode) from grid nodes: tree t's grid nodes
+// [roots[t], roots[t+1]) map to walk nodes [wroots[t], ...) in the same order.
+__global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t n, const int32_t* __restrict__ roots,
+                                        int32_t n_trees, const int32_t* __restrict__ wroots,
+                                        const double* __restrict__ thr, const int32_t* __restrict__ thr_off,
+                                        WNode* __restrict__ dst) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int32_t lo = 0, hi = n_trees - 1;  // last tree with roots[t] <= i
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(roots + mid) <= i) lo = mid;
+            else hi = mid - 1;
+        }
+        const int32_t root = __ldg(roots + lo);
+        const PNode x = grid[i];
+        WNode w;
+        if (x.feat == kFeatLeaf) {
+            w.key = static_cast<int32_t>(i);
+            w.fc = static_cast<int32_t>(0xffff0000u);
+        } else {
+            const int32_t child = x.aux - root;
+            if (x.feat < 0) {
+                w.key = static_cast<int32_t>(t16_of(x.v));
+            } else {
+                const int32_t o = __ldg(thr_off + x.feat), c = __ldg(thr_off + x.feat + 1) - o;
+                const int32_t r = rank_of(thr + o, c, x.v);
+                w.key = (x.v == x.v && r < c) ? r : -1;  // exact match; NaN thresholds never pass
+            }
+            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 16) | static_cast<uint32_t>(child));
+        }
+        dst[__ldg(wroots + lo) + (i - root)] = w;
     }
 }
 
@@ -201,6 +238,17 @@ int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t s
     if (blocks > 8192) blocks = 8192;
     if (blocks < 1) blocks = 1;
     recode_clock_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n, sm_col, mem_col);
+    return cudaGetLastError();
+}
+
+int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
+                            const int32_t* wroots, const double* thr, const int32_t* thr_off, WNode* dst,
+                            void* stream) {
+    int blocks = static_cast<int>((n + 255) / 256);
+    if (blocks > 8192) blocks = 8192;
+    if (blocks < 1) blocks = 1;
+    build_walk_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(grid, n, roots, n_trees, wroots,
+                                                                                  thr, thr_off, dst);
     return cudaGetLastError();
 }
 

@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """Per-CUDA-source-line instruction and stall totals from an ncu report.
 
-    python scripts/ncu_lines.py report.ncu-rep [--top N]
+    python scripts/ncu_lines.py report.ncu-rep [--top N] [--kernel REGEX]
 """
 import csv, io, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--print-source", "cuda,sass", "--csv"],
+kern = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else None
+kf = ["-k", f"regex:{kern}"] if kern else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--print-source", "cuda,sass", "--csv"],
                      capture_output=True, text=True).stdout
 rows, cur_file, hdr = [], None, None
 for r in csv.reader(io.StringIO(out)):

@@ -1,18 +1,25 @@
 #!/usr/bin/env python
 """Per-opcode and per-region breakdown of an ncu source page (SASS view).
 
-    python scripts/ncu_sass.py report.ncu-rep [--top N]
+    python scripts/ncu_sass.py report.ncu-rep [--top N] [--kernel REGEX] [--dump FILE]
 """
 import collections, csv, io, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
-lines = out.splitlines()
-rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
-hdr = rows[0]
+kern = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else None
+kf = ["-k", f"regex:{kern}"] if kern else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+rows = [r for r in csv.reader(io.StringIO(out)) if r]
+hi = next(i for i, r in enumerate(rows) if "Instructions Executed" in r)
+hdr = rows[hi]
+rows = rows[hi:]
 ix = {h: i for i, h in enumerate(hdr)}
-body = [r for r in rows[1:] if len(r) == len(hdr)]
+body = [r for r in rows[1:] if len(r) == len(hdr) and r[0] != hdr[0]]
+if "--dump" in sys.argv:
+    with open(sys.argv[sys.argv.index("--dump") + 1], "w") as fh:
+        for r in body:
+            fh.write(f"{float(r[ix['Instructions Executed']] or 0):12.0f} {float(r[ix['Warp Stall Sampling (All Samples)']] or 0):6.0f}  {r[ix['Source']].strip()}\n")
 ie, st, th = ix["Instructions Executed"], ix["Warp Stall Sampling (All Samples)"], ix["Avg. Threads Executed"]
 tot_i = sum(float(r[ie] or 0) for r in body)
 tot_s = sum(float(r[st] or 0) for r in body)
