@@ -49,13 +49,16 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4 };
 
-// One (app, tree) record.  info = kind | t16 << 16 (SM / MEM keys).
-//   CONST: v = leaf value.              SM/MEM: v = left leaf, ref = right leaf node.
-//   TABLE: ref = residue-table index.   FULL:   ref = first clock node.
+// One (app, tree) record.  info = kind | t16 << 16 (SM / MEM keys); leaves
+// are referenced by packed (grid) index and their values fetched by the
+// accumulate kernel's prefetch stage.
+//   CONST: ref = the leaf.                 SM/MEM: ref / ref2 = left / right leaf.
+//   TABLE: ref = residue-table index.      FULL:   ref = first clock node.
 struct __align__(16) TreeRec {
-    double v;
     uint32_t info;
     int32_t ref;
+    int32_t ref2;
+    uint32_t pad;
 };
 static_assert(sizeof(TreeRec) == 16, "TreeRec is 16 bytes");
 
@@ -235,15 +238,14 @@ __device__ __forceinline__ Walk child_walk(const Walk& w, int side) { return Wal
 template <bool kAllSmem>
 __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const WalkCtx& c, const TreeSrc& s,
                                                    const Walk& w) {
-    TreeRec r;
-    r.v = 0.0;
+    TreeRec r{0u, 0, 0, 0u};
     Walk A = child_walk(w, 0), B = child_walk(w, 1);
     walk2<kAllSmem>(c, s, true, A, true, B);
     const bool ac = A.fc < 0 && wfeat(A.fc) != kFeatLeaf, bc = B.fc < 0 && wfeat(B.fc) != kFeatLeaf;
     if (!ac && !bc) {
-        r.v = leaf_value(c, A);
         r.info = (wfeat(w.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w.key) << 16);
-        r.ref = B.key;
+        r.ref = A.key;
+        r.ref2 = B.key;
         return r;
     }
     r.info = kRecFull;
@@ -344,13 +346,7 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
                                             int& count, int lane, bool v, const Walk& w, int32_t t, uint32_t saddr,
                                             int li, int model, TreeRec* out, int64_t tile0) {
     const bool job = v && wfeat(w.fc) != kFeatLeaf;
-    if (v && !job) {
-        TreeRec r;
-        r.v = leaf_value(c, w);
-        r.info = kRecConst;
-        r.ref = 0;
-        out[rec_index(t, tile0 + li, p.n_apps)] = r;
-    }
+    if (v && !job) out[rec_index(t, tile0 + li, p.n_apps)] = TreeRec{kRecConst, w.key, 0, 0u};
     const unsigned m = __ballot_sync(kFull, job);
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, saddr, li};
     count += __popc(m);
@@ -417,19 +413,29 @@ __device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, in
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Bounded spin: a barrier that never completes is a bug -- trap (the launch
+// fails) instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
+    for (uint32_t spins = 0;; ++spins) {
+        uint32_t done;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (spins > (1u << 26)) __trap();
+    }
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -496,35 +502,48 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
     const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
 
+    // Barriers: full[b] (thread 0's arrive + the stage's TMA bytes) at bar0
+    // + 8b, empty[b] (one arrive per warp once done with the stage) at bar0 +
+    // 16 + 8b.  Warps run decoupled; thread 0 refills a buffer only after
+    // every warp released it.
+    const int nwarps = blockDim.x >> 5;
     int32_t cur_it = it_begin, cur_q = -1;  // thread 0's schedule cursor
     if (threadIdx.x == 0) {
         mbar_init(bar0, 1);
         mbar_init(bar0 + 8, 1);
+        mbar_init(bar0 + 16, nwarps);
+        mbar_init(bar0 + 24, nwarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const Stage s = next_stage(p, it_end, cur_it, cur_q);
         desc[0] = s;
         if (s.valid) issue_stage(p, s, bufs0, bar0, tables);
+        else mbar_arrive(bar0);
     }
-    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    __syncthreads();
     int32_t row_tile = -1, row_model = -1;
     for (int k = 0;; ++k) {
         const int buf = k & 1;
-        __syncthreads();  // stage k-1 is done: buffer buf ^ 1 and its table are free
-        const Stage s = desc[buf];
-        if (!s.valid) break;
+        const uint32_t use = static_cast<uint32_t>(k >> 1) & 1u;  // parity of this use of buffer `buf`
         if (threadIdx.x == 0) {
-            // Plan and load stage k + 1 while the CTA walks stage k.
+            // Refill the other buffer with stage k + 1 once stage k - 1 is released.
+            if (k >= 1) mbar_wait(bar0 + 16 + 8 * (buf ^ 1), static_cast<uint32_t>((k - 1) >> 1) & 1u);
             const Stage nx = next_stage(p, it_end, cur_it, cur_q);
             desc[buf ^ 1] = nx;
             if (nx.valid) {
                 issue_stage(p, nx, bufs0 + static_cast<uint32_t>((buf ^ 1) * buf_bytes), bar0 + 8 * (buf ^ 1),
                             tables + (buf ^ 1) * kStageTrees);
+            } else {
+                mbar_arrive(bar0 + 8 * (buf ^ 1));
             }
         }
+        mbar_wait(bar0 + 8 * buf, use);
+        const Stage s = desc[buf];
+        if (!s.valid) break;
         const ItemInfo ii = item_info(p, s.item);
         const int64_t tile0 = static_cast<int64_t>(ii.tile) * TA;
         const int n_here = static_cast<int>(min(static_cast<int64_t>(TA), p.n_apps - tile0));
         if (ii.tile != row_tile || ii.model != row_model) {
+            __syncthreads();  // every warp is done with the previous tile's ranks
             // Stage the tile's ranks transposed: srank[col * TA + app].
             const int F = p.n_cols;
             const uint16_t* src = p.ranks + (static_cast<int64_t>(ii.model) * p.n_apps + tile0) * F;
@@ -536,8 +555,6 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
             row_tile = ii.tile;
             row_model = ii.model;
         }
-        mbar_wait(bar0 + 8 * buf, (phase >> buf) & 1u);
-        phase ^= 1u << buf;
 
         const int li = group * 32 + lane;
         const bool valid = li < n_here;
@@ -578,6 +595,8 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
                                       out, tile0);
         }
         if (count > 0) run_jobs<kAllSmem>(p, c0, jobs, count, lane, ii.model, out, tile0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar0 + 16 + 8 * buf);  // this warp is done with buffer `buf`
     }
 }
 
@@ -620,12 +639,12 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
 constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kAccThreads = kAccWarps * 32;
 
-// Per-warp shared region: value ring [3][32] | meta ring [3][32] | right-leaf
-// values [2][32] | residue-table slots [2][kSide] | overflow slot | row.
+// Per-warp shared region: record ring [3][32] | leaf values [2][32] | right
+// leaf values [2][32] | residue-table slots [2][kSide] | overflow slot | row.
 constexpr int kSide = 8;
-constexpr int kOffVal = 0;
-constexpr int kOffMeta = kOffVal + 3 * 32 * 8;
-constexpr int kOffRv = kOffMeta + 3 * 32 * 8;
+constexpr int kOffMeta = 0;
+constexpr int kOffVal = kOffMeta + 3 * 32 * 16;
+constexpr int kOffRv = kOffVal + 2 * 32 * 8;
 constexpr int kOffSide = kOffRv + 2 * 32 * 8;
 constexpr int kOffOvf = kOffSide + 2 * kSide * 128;
 constexpr int kOffRow = kOffOvf + 128;
@@ -680,39 +699,41 @@ __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nod
     }
 }
 
-// Stage 1 of the ring: the value and meta words of tree g*32 + lane.
+// Stage 1 of the ring: the record of tree g*32 + lane.
 __device__ __forceinline__ void issue_rec(const AccModel& m, int64_t la, int64_t n_apps, int g, int lane,
                                           uint32_t ws) {
     const int32_t t = g * 32 + lane;
     if (t < m.n_trees) {
-        const TreeRec* src = m.rec + rec_index(t, la, n_apps);
-        const uint32_t slot = static_cast<uint32_t>(((g % 3) * 32 + lane) * 8);
-        cp_async8(ws + kOffVal + slot, &src->v);
-        cp_async8(ws + kOffMeta + slot, &src->info);
+        cp_async16(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16), m.rec + rec_index(t, la, n_apps));
     }
 }
 
-// Stage 2: the side data the record points at (right leaf value / residue
-// table).  Returns the group's residue-table mask (slot = rank in it).
-__device__ __forceinline__ unsigned issue_side(const AccModel& m, const RTRec* __restrict__ pool, int g, int lane,
-                                               uint32_t ws) {
+// Stage 2: what the record points at -- leaf values (CONST, SM / MEM) or the
+// residue table (staged into slot = rank among the group's tables).
+__device__ __forceinline__ void issue_side(const AccModel& m, const RTRec* __restrict__ pool, int g, int lane,
+                                           uint32_t ws) {
     const int32_t t = g * 32 + lane;
-    uint2 meta = make_uint2(kRecConst, 0u);
-    if (t < m.n_trees) meta = lds_u2(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 8));
-    const uint32_t kind = meta.x & 7u;
+    uint32_t kind = kRecFull, ref = 0, ref2 = 0;
+    if (t < m.n_trees) {
+        const uint32_t a = ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16);
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(kind), "=r"(ref) : "r"(a));
+        ref2 = lds_u32(a + 8u);
+        kind &= 7u;
+    }
     const unsigned tm = __ballot_sync(kFull, kind == kRecTable);
-    if (kind == kRecSm || kind == kRecMem) {
-        cp_async8(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + lane) * 8), &m.nodes[static_cast<int32_t>(meta.y)].v);
+    const uint32_t vslot = static_cast<uint32_t>(((g & 1) * 32 + lane) * 8);
+    if (kind == kRecConst || kind == kRecSm || kind == kRecMem) {
+        cp_async8(ws + kOffVal + vslot, &m.nodes[static_cast<int32_t>(ref)].v);
+        if (kind != kRecConst) cp_async8(ws + kOffRv + vslot, &m.nodes[static_cast<int32_t>(ref2)].v);
     } else if (kind == kRecTable) {
         const int slot = __popc(tm & ((1u << lane) - 1u));
         if (slot < kSide) {
-            const unsigned char* src = reinterpret_cast<const unsigned char*>(pool + meta.y);
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(pool + ref);
             const uint32_t dst = ws + kOffSide + static_cast<uint32_t>(((g & 1) * kSide + slot) * 128);
 #pragma unroll
             for (int k = 0; k < 8; ++k) cp_async16(dst + 16 * k, src + 16 * k);
         }
     }
-    return tm;
 }
 
 template <int CPL>
@@ -749,19 +770,20 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
                                             int j, const GroupMasks& gm, const double* row,
                                             const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l, int lane,
                                             double (&acc)[CPL]) {
-    const uint32_t slotb = static_cast<uint32_t>(((g % 3) * 32 + j) * 8);
+    const uint32_t slotb = static_cast<uint32_t>(((g % 3) * 32 + j) * 16);
+    const uint32_t vslot = static_cast<uint32_t>(((g & 1) * 32 + j) * 8);
     const unsigned bit = 1u << j;
     if (gm.sm & bit) {
         const uint32_t info = lds_u32(ws + kOffMeta + slotb);
-        const double lv = lds_f64(ws + kOffVal + slotb);
-        const double rv = lds_f64(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + j) * 8));
+        const double lv = lds_f64(ws + kOffVal + vslot);
+        const double rv = lds_f64(ws + kOffRv + vslot);
         const unsigned key = (info & 0xffff0000u) | 0xffffu;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= key ? lv : rv);
     } else if (gm.mem & bit) {
         const uint32_t info = lds_u32(ws + kOffMeta + slotb);
-        const double lv = lds_f64(ws + kOffVal + slotb);
-        const double rv = lds_f64(ws + kOffRv + static_cast<uint32_t>(((g & 1) * 32 + j) * 8));
+        const double lv = lds_f64(ws + kOffVal + vslot);
+        const double rv = lds_f64(ws + kOffRv + vslot);
         const unsigned key = info >> 16;
         if (mem_uniform) {  // all of this lane's clocks share one memory clock
             add_const<CPL>(acc, mem_l <= key ? lv : rv);
@@ -818,8 +840,8 @@ __device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec*
         cp_async_commit();
 
         const int nth = min(32, m.n_trees - g * 32);
-        const uint32_t vals = ws + kOffVal + static_cast<uint32_t>((g % 3) * 32 * 8);
-        const uint32_t kind_l = lane < nth ? (lds_u32(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 8)) & 7u)
+        const uint32_t vals = ws + kOffVal + static_cast<uint32_t>((g & 1) * 32 * 8);
+        const uint32_t kind_l = lane < nth ? (lds_u32(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16)) & 7u)
                                            : kRecConst;
         GroupMasks gm;
         gm.nc = __ballot_sync(kFull, kind_l != kRecConst);
