@@ -120,6 +120,7 @@ struct WalkParams {
     int32_t n_items;           // tiles * 2 * splits, tile-major
     int32_t win_nodes;         // per-tree window staged in shared memory (BFS prefix, even)
     int32_t stage_nodes;       // capacity of one stage buffer (walk nodes)
+    int32_t n_bufs;            // stage buffers in the ring (2..4)
     TreeRec* rec[2];
     RTRec* pool;
     uint32_t* pool_count;
@@ -378,13 +379,11 @@ __device__ __forceinline__ ItemInfo item_info(const WalkParams& p, int32_t it) {
     return r;
 }
 
-__device__ __forceinline__ int32_t tree_window(const WalkParams& p, const int32_t* wroots, int32_t t) {
-    return min(__ldg(wroots + t + 1) - __ldg(wroots + t), p.win_nodes);
-}
 
-// Thread 0: the next stage after cursor (it, q), advancing the cursor.
-__device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q) {
-    Stage s{0, 0, 0, 0};
+// Warp 0 (all lanes, uniform result): the next stage after cursor (it, q),
+// advancing the cursor.  Lane l sizes pair q + l; a stage is the longest
+// prefix of up to 32 pairs whose windows fit one buffer (at least one pair).
+__device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q, int lane) {
     while (it < it_end) {
         const ItemInfo ii = item_info(p, it);
         if (q < ii.p0) q = ii.p0;
@@ -395,19 +394,26 @@ __device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, in
         }
         const int32_t nt = p.n_trees[ii.model];
         const int32_t* wroots = p.wroots[ii.model];
-        int32_t used = 0, qe = q;
-        while (qe < ii.p1) {
-            int32_t w = tree_window(p, wroots, 2 * qe);
-            if (2 * qe + 1 < nt) w += tree_window(p, wroots, 2 * qe + 1);
-            if (qe > q && (used + w > p.stage_nodes || 2 * (qe - q + 1) > kStageTrees)) break;
-            used += w;
-            ++qe;
+        const int32_t pr = q + lane;
+        int32_t w = 1 << 20;  // > any stage; 32 of them cannot overflow
+        if (pr < ii.p1) {
+            const int32_t r0 = __ldg(wroots + 2 * pr), r1 = __ldg(wroots + min(2 * pr + 1, nt)),
+                          r2 = __ldg(wroots + min(2 * pr + 2, nt));
+            w = min(r1 - r0, p.win_nodes) + min(r2 - r1, p.win_nodes);
         }
-        s = Stage{it, q, qe, 1};
-        q = qe;
+        int32_t incl = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t o = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const bool fits = lane == 0 || (incl <= p.stage_nodes && 2 * (lane + 1) <= kStageTrees);
+        const int n = __popc(__ballot_sync(kFull, fits));
+        const Stage s{it, q, q + n, 1};
+        q += n;
         return s;
     }
-    return s;
+    return Stage{0, 0, 0, 0};
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -443,36 +449,47 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 
-// Thread 0: load the windows of stage s into buffer `buf` (adjacent whole
-// trees in one bulk copy), arm its barrier and fill the stage's tree table
-// {walk root, grid root, window nodes, shared address}.
-__device__ void issue_stage(const WalkParams& p, const Stage& s, uint32_t buf_saddr, uint32_t bar, int4* table) {
+// Warp 0: load the windows of stage s into its buffer and arm the buffer's
+// barrier; lane i fills tree 2*q0 + i's table entry {walk root, grid root,
+// window nodes, shared address}.  Whole trees are contiguous, so with
+// kAllSmem the stage is one bulk copy; otherwise each lane copies its window.
+template <bool kAllSmem>
+__device__ void issue_stage(const WalkParams& p, const Stage& s, uint32_t buf_saddr, uint32_t bar, int4* table,
+                            int lane) {
     const ItemInfo ii = item_info(p, s.item);
     const int32_t nt = p.n_trees[ii.model];
     const int32_t* wroots = p.wroots[ii.model];
     const int32_t* roots = p.roots[ii.model];
     const WNode* nodes = p.wnodes[ii.model];
-    uint32_t bytes = 0;
-    for (int32_t t = 2 * s.q0; t < 2 * s.q1 && t < nt; ++t) bytes += 8u * tree_window(p, wroots, t);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, bytes);
-    uint32_t off = 0, run = 0;
-    const WNode* run_src = nullptr;
-    for (int32_t t = 2 * s.q0; t < 2 * s.q1 && t < nt; ++t) {
-        const int32_t wr = __ldg(wroots + t);
-        const int32_t win = tree_window(p, wroots, t);
-        const uint32_t w = 8u * static_cast<uint32_t>(win);
-        const WNode* src = nodes + wr;
-        if (run > 0 && reinterpret_cast<const char*>(run_src) + run != reinterpret_cast<const char*>(src)) {
-            bulk_g2s(buf_saddr + off - run, run_src, run, bar);
-            run = 0;
+    const int32_t t_end = min(2 * s.q1, nt);
+    uint32_t total = 0;
+    for (int32_t t0 = 2 * s.q0; t0 < t_end; t0 += 32) {
+        const int32_t t = t0 + lane;
+        const bool has = t < t_end;
+        const int32_t wr = has ? __ldg(wroots + t) : 0;
+        const int32_t win = has ? min(__ldg(wroots + t + 1) - wr, p.win_nodes) : 0;
+        int32_t incl = win;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t o = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += o;
         }
-        if (run == 0) run_src = src;
-        table[t - 2 * s.q0] = make_int4(wr, __ldg(roots + t), win, static_cast<int>(buf_saddr + off));
-        run += w;
-        off += w;
+        const uint32_t off = total + 8u * static_cast<uint32_t>(incl - win);
+        if (has) {
+            table[t - 2 * s.q0] = make_int4(wr, __ldg(roots + t), win, static_cast<int>(buf_saddr + off));
+            if (!kAllSmem) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bulk_g2s(buf_saddr + off, nodes + wr, 8u * static_cast<uint32_t>(win), bar);
+            }
+        }
+        total += 8u * static_cast<uint32_t>(__shfl_sync(kFull, incl, 31));
     }
-    if (run > 0) bulk_g2s(buf_saddr + off - run, run_src, run, bar);
+    __syncwarp();  // the table entries are visible before lane 0's arrive releases them
+    if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (kAllSmem) bulk_g2s(buf_saddr, nodes + __ldg(wroots + 2 * s.q0), total, bar);
+        mbar_expect_tx(bar, total);
+    }
 }
 
 // Shared layout: barriers + stage descriptors | buffer 0 | buffer 1 | ranks
@@ -493,50 +510,55 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     const int TA = p.tile_apps, groups = TA >> 5;
     const int group = warp % groups, sub = warp / groups;
     const size_t buf_bytes = static_cast<size_t>(p.stage_nodes) * 8;
-    Stage* desc = reinterpret_cast<Stage*>(smem + 16);
+    const int NB = p.n_bufs;
+    // Header: full[b] at bar0 + 8b, empty[b] at bar0 + 32 + 8b, stage
+    // descriptors at +64 (NB <= 4).
+    Stage* desc = reinterpret_cast<Stage*>(smem + 64);
     const uint32_t bar0 = smem_addr(smem), bufs0 = smem_addr(smem + 128);
-    uint16_t* srank = reinterpret_cast<uint16_t*>(smem + 128 + 2 * buf_bytes);
-    unsigned char* after_ranks = smem + 128 + 2 * buf_bytes + walk_rank_bytes(p.n_cols, TA);
+    uint16_t* srank = reinterpret_cast<uint16_t*>(smem + 128 + NB * buf_bytes);
+    unsigned char* after_ranks = smem + 128 + NB * buf_bytes + walk_rank_bytes(p.n_cols, TA);
     Job* jobs = reinterpret_cast<Job*>(after_ranks) + warp * kJobCap;
     int4* tables = reinterpret_cast<int4*>(after_ranks + walk_jobs_bytes(blockDim.x >> 5));
     const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
     const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
 
-    // Barriers: full[b] (thread 0's arrive + the stage's TMA bytes) at bar0
-    // + 8b, empty[b] (one arrive per warp once done with the stage) at bar0 +
-    // 16 + 8b.  Warps run decoupled; thread 0 refills a buffer only after
-    // every warp released it.
+    // full[b]: thread 0's arrive + the stage's TMA bytes; empty[b]: one arrive
+    // per warp once done with the stage.  Warps run decoupled; thread 0
+    // refills a buffer (NB - 1 stages ahead) only after every warp released it.
     const int nwarps = blockDim.x >> 5;
-    int32_t cur_it = it_begin, cur_q = -1;  // thread 0's schedule cursor
+    int32_t cur_it = it_begin, cur_q = -1;  // warp 0's schedule cursor
+    auto produce = [&](int j) {  // warp 0: plan stage j into buffer j % NB
+        const int b = j % NB;
+        const Stage nx = next_stage(p, it_end, cur_it, cur_q, lane);
+        if (lane == 0) desc[b] = nx;
+        if (nx.valid) {
+            issue_stage<kAllSmem>(p, nx, bufs0 + static_cast<uint32_t>(b * buf_bytes), bar0 + 8 * b,
+                                  tables + b * kStageTrees, lane);
+        } else if (lane == 0) {
+            mbar_arrive(bar0 + 8 * b);
+        }
+    };
     if (threadIdx.x == 0) {
-        mbar_init(bar0, 1);
-        mbar_init(bar0 + 8, 1);
-        mbar_init(bar0 + 16, nwarps);
-        mbar_init(bar0 + 24, nwarps);
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(bar0 + 8 * b, 1);
+            mbar_init(bar0 + 32 + 8 * b, nwarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const Stage s = next_stage(p, it_end, cur_it, cur_q);
-        desc[0] = s;
-        if (s.valid) issue_stage(p, s, bufs0, bar0, tables);
-        else mbar_arrive(bar0);
     }
     __syncthreads();
+    if (warp == 0) {
+        for (int j = 0; j + 1 < NB; ++j) produce(j);
+    }
     int32_t row_tile = -1, row_model = -1;
     for (int k = 0;; ++k) {
-        const int buf = k & 1;
-        const uint32_t use = static_cast<uint32_t>(k >> 1) & 1u;  // parity of this use of buffer `buf`
-        if (threadIdx.x == 0) {
-            // Refill the other buffer with stage k + 1 once stage k - 1 is released.
-            if (k >= 1) mbar_wait(bar0 + 16 + 8 * (buf ^ 1), static_cast<uint32_t>((k - 1) >> 1) & 1u);
-            const Stage nx = next_stage(p, it_end, cur_it, cur_q);
-            desc[buf ^ 1] = nx;
-            if (nx.valid) {
-                issue_stage(p, nx, bufs0 + static_cast<uint32_t>((buf ^ 1) * buf_bytes), bar0 + 8 * (buf ^ 1),
-                            tables + (buf ^ 1) * kStageTrees);
-            } else {
-                mbar_arrive(bar0 + 8 * (buf ^ 1));
-            }
+        const int buf = k % NB;
+        if (warp == 0) {
+            // Refill the buffer of stage k - 1 with stage k + NB - 1 once every warp released it.
+            if (k >= 1) mbar_wait(bar0 + 32 + 8 * ((k - 1) % NB), static_cast<uint32_t>((k - 1) / NB) & 1u);
+            produce(k + NB - 1);
+            __syncwarp();
         }
-        mbar_wait(bar0 + 8 * buf, use);
+        mbar_wait(bar0 + 8 * buf, static_cast<uint32_t>(k / NB) & 1u);
         const Stage s = desc[buf];
         if (!s.valid) break;
         const ItemInfo ii = item_info(p, s.item);
@@ -596,7 +618,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         }
         if (count > 0) run_jobs<kAllSmem>(p, c0, jobs, count, lane, ii.model, out, tile0);
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar0 + 16 + 8 * buf);  // this warp is done with buffer `buf`
+        if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`
     }
 }
 
@@ -1157,7 +1179,7 @@ int launch_acc_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
 // Walk-kernel geometry: warps per CTA (two per 32 apps) so the transposed
 // ranks plus two stage buffers of tree windows fit the opt-in shared memory.
 struct WalkGeom {
-    int warps, win_nodes, stage_nodes;
+    int warps, win_nodes, stage_nodes, n_bufs;
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
@@ -1165,18 +1187,20 @@ WalkGeom walk_geom(const GridParams& p) {
     constexpr size_t kLimit = 227 * 1024;
     WalkGeom g{};
     g.win_nodes = static_cast<int>(env_i64("GDVFS_WIN_NODES", 512)) & ~1;
+    g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
+    g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
     if (g.win_nodes < 2) g.win_nodes = 2;
     const int32_t max_pair = (p.e_max_pair_nodes > p.t_max_pair_nodes ? p.e_max_pair_nodes : p.t_max_pair_nodes) + 2;
     const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
     for (int groups = 8; groups >= 1; groups >>= 1) {
         const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(2 * groups) +
-                             2 * kStageTrees * 16;
-        if (fixed + 2 * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
+                             static_cast<size_t>(g.n_bufs) * kStageTrees * 16;
+        if (fixed + g.n_bufs * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
         g.warps = 2 * groups;
-        int64_t stage = static_cast<int64_t>((kLimit - fixed) / 16) & ~1;
+        int64_t stage = static_cast<int64_t>((kLimit - fixed) / (8 * g.n_bufs)) & ~1;
         if (stage > 16384) stage = 16384;
         g.stage_nodes = static_cast<int>(stage);
-        g.smem = fixed + 2 * static_cast<size_t>(g.stage_nodes) * 8;
+        g.smem = fixed + g.n_bufs * static_cast<size_t>(g.stage_nodes) * 8;
         return g;
     }
     g.warps = 0;  // too many columns
@@ -1280,6 +1304,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.tile_apps = wg.warps * 16;
         w.win_nodes = wg.win_nodes;
         w.stage_nodes = wg.stage_nodes;
+        w.n_bufs = wg.n_bufs;
         w.rec[0] = rec_e;
         w.rec[1] = rec_t;
         w.pool = pool;
