@@ -355,7 +355,10 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
     if (count >= 32) run_jobs<kAllSmem>(p, c0, jobs, count, lane, model, out, tile0);
 }
 
-constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
+constexpr int kStageTrees = 128;
+#ifndef GD_WALK_NW
+#define GD_WALK_NW 4  // independent walks per lane in the root-walk loop
+#endif  // trees per stage (table entries per buffer)
 
 // One stage of the CTA's schedule.
 struct Stage {
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         int count = 0;
         // This warp walks trees 2q + sub of four consecutive pairs side by side.
         const int4* table = tables + buf * kStageTrees;
-        constexpr int NW = 4;
+        constexpr int NW = GD_WALK_NW;
         const int32_t t_last = min(2 * s.q1, nt) - 1;
         for (int32_t q = s.q0; q < s.q1; q += NW) {
             TreeSrc src[NW];
@@ -1192,7 +1195,9 @@ WalkGeom walk_geom(const GridParams& p) {
     if (g.win_nodes < 2) g.win_nodes = 2;
     const int32_t max_pair = (p.e_max_pair_nodes > p.t_max_pair_nodes ? p.e_max_pair_nodes : p.t_max_pair_nodes) + 2;
     const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
+    const int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 8));
     for (int groups = 8; groups >= 1; groups >>= 1) {
+        if (groups > max_groups) continue;
         const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(2 * groups) +
                              static_cast<size_t>(g.n_bufs) * kStageTrees * 16;
         if (fixed + g.n_bufs * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
