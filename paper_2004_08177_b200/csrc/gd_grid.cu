@@ -1217,11 +1217,19 @@ int64_t env_i64(const char* name, int64_t dflt) {
     return e ? std::atoll(e) : dflt;
 }
 
+// Residue-table capacity per app: 1/8 of the trees (GDVFS_POOL_DIV overrides
+// the divisor; overflowing tables fall back to FULL records).
+int64_t pool_per_app(const GridParams& p) {
+    int64_t div = env_i64("GDVFS_POOL_DIV", 8);
+    if (div < 1) div = 1;
+    return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 1;
+}
+
 // Apps per batch: the walk records of one batch stay bounded (and, at the
 // default budget, mostly L2-resident between the two kernels).
 int64_t batch_apps(const GridParams& p) {
     const int64_t per_app = grid_scratch_per_app(p);
-    static const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 31);
+    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 31);
     int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
     b = b < 256 ? 256 : b;
     return b < p.n_apps ? b : p.n_apps;
@@ -1231,7 +1239,7 @@ int64_t batch_apps(const GridParams& p) {
 
 int64_t grid_scratch_per_app(const GridParams& p) {
     const int64_t pairs = ((p.e_trees + 1) >> 1) + ((p.t_trees + 1) >> 1);
-    const int64_t pool = (static_cast<int64_t>(p.e_trees) + p.t_trees) / 8 + 1;  // residue tables per app
+    const int64_t pool = pool_per_app(p);  // residue tables per app
     const int64_t ranks = (2LL * p.n_cols * 2 + 15) & ~15LL;
     return pairs * 2 * static_cast<int64_t>(sizeof(TreeRec)) + pool * static_cast<int64_t>(sizeof(RTRec)) + ranks;
 }
@@ -1264,7 +1272,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     const int64_t B = batch_apps(p);
     const int64_t nb = (p.n_apps + B - 1) / B;
     const int64_t pe = (p.e_trees + 1) >> 1, pt = (p.t_trees + 1) >> 1;
-    const int64_t pool_cap = B * ((static_cast<int64_t>(p.e_trees) + p.t_trees) / 8 + 1);
+    const int64_t pool_cap = B * pool_per_app(p);
     unsigned char* base = static_cast<unsigned char*>(scratch);
     TreeRec* rec_e = reinterpret_cast<TreeRec*>(base);
     TreeRec* rec_t = rec_e + B * pe * 2;

@@ -129,6 +129,59 @@ def test_k2_grid_predictions_and_decisions_vs_oracle(ctx, name):
         assert decisions_equal(got, want), (name, combo)
 
 
+# Internal paths of the walk / accumulate pipeline forced through knobs (the
+# library reads them per call): several batches, small shared-memory windows
+# (walks continue from global memory), residue-table pool overflow (FULL
+# records), deeper buffer rings, one app group per CTA.
+KNOBS = {
+    "batches": {"GDVFS_BATCH_BYTES": "300000"},
+    "windowed": {"GDVFS_WIN_NODES": "16"},
+    "pool_overflow": {"GDVFS_POOL_DIV": "1000000"},
+    "ring4": {"GDVFS_WALK_BUFS": "4"},
+    "one_group": {"GDVFS_WALK_GROUPS": "1", "GDVFS_WALK_BUFS": "3"},
+}
+
+
+@pytest.mark.parametrize("knob", list(KNOBS))
+def test_k2_internal_paths_vs_oracle(ctx, knob, monkeypatch):
+    for k, v in KNOBS[knob].items():
+        monkeypatch.setenv(k, v)
+    sc = W.make_scenario(knob, 700, "gtx980", 90, 9, seed=23, w_clk=0.08)
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=9)
+    want, we, wt = O.oracle_grid(sc.energy, sc.time, sc.grid, budgets)
+    got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
+    assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+    assert decisions_equal(got, want)
+
+
+@pytest.mark.parametrize("n_mem", [1, 4, 31, 32, 40])
+def test_k2_clock_lane_maps(ctx, n_mem):
+    # Catalogs whose memory-clock runs fit 32 lanes use the per-lane uniform
+    # memory clock layout; more runs than lanes fall back to contiguous slots.
+    rng = np.random.default_rng(n_mem)
+    mems = np.sort(rng.choice(np.arange(300, 4000), size=n_mem, replace=False))
+    per = max(1, 96 // n_mem)
+    pairs = sorted({(int(sm), int(m)) for m in mems for sm in rng.choice(np.arange(300, 2000), size=per)},
+                   key=lambda p: (p[1], p[0]))
+    sm = np.array([p[0] for p in pairs], np.int32)
+    mem = np.array([p[1] for p in pairs], np.int32)
+    sc = W.make_scenario("map", 96, "gtx980", 40, 8, seed=n_mem, w_clk=0.3)
+    cols = W._ColumnModel(np.random.default_rng(1), W.N_COLS, W.CAT_COLS, sm, mem, W.SM_COL, W.MEM_COL)
+    fe = W.make_forest(cols, 40, 8, 0, 5, w_clk=0.3)
+    ft = W.make_forest(cols, 40, 8, 1, 6, w_clk=0.3)
+    g = W.GridInputs(sc.grid.rows, sc.grid.cat_t, sc.grid.cat_cols, sm, mem, W.SM_COL, W.MEM_COL)
+    me, mt = gd.Model.from_forest(fe, ctx), gd.Model.from_forest(ft, ctx)
+    _, _, t0 = O.oracle_grid(fe, ft, g, np.ones(g.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=2)
+    for combo in ((0, 1, 0, 0), (1, 1, 1, 1)):
+        want, we, wt = O.oracle_grid(fe, ft, g, budgets, combo[0], combo[2], combo[3])
+        got, ge, gt = gd.grid_select(me, mt, g, budgets, opts_of(*combo), return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt)), combo
+        assert decisions_equal(got, want), combo
+
+
 def test_k2_general_mode_c1_golden(ctx):
     # Per-clock records (nearest-record substitution, scheduler.cpp:341-359):
     # predictions must equal the reference's ClockPredictor outputs bit for bit.
