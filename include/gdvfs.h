@@ -148,6 +148,13 @@ int gd_ctx_set_stream(gd_ctx* ctx, void* cuda_stream);
 int gd_ctx_synchronize(gd_ctx* ctx);
 /* Number of kernels this context has launched so far. */
 int64_t gd_ctx_launch_count(const gd_ctx* ctx);
+/* Per-kernel timing (measurement hook, off by default): while on, every grid
+ * call records CUDA events on the context stream around each kernel it
+ * launches; gd_ctx_kernel_times then synchronizes on them and returns the
+ * last grid call's kernel durations in launch order (ms) with their kernel
+ * names ("rank", "walk", "acc" per app batch, or "general"), n = count. */
+int gd_ctx_set_timing(gd_ctx* ctx, int on);
+int gd_ctx_kernel_times(gd_ctx* ctx, float* ms, const char** names, int32_t max, int32_t* n);
 
 /* Models: the packer.  Replaces holding a models::FittedModel
  * (models.hpp:63-70) for prediction.  Validates the trees (children in range,

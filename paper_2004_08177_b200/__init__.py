@@ -113,6 +113,19 @@ class Context:
     def launch_count(self) -> int:
         return int(_capi.lib().gd_ctx_launch_count(self._h))
 
+    def set_timing(self, on: bool) -> None:
+        """Measurement hook: record CUDA events around each grid kernel."""
+        _raise(_capi.lib().gd_ctx_set_timing(self._h, int(bool(on))))
+
+    def kernel_times(self):
+        """[(kernel name, ms)] of the last grid call (synchronizes on its events)."""
+        n = C.c_int32(0)
+        _raise(_capi.lib().gd_ctx_kernel_times(self._h, None, None, 0, C.byref(n)))
+        ms = (C.c_float * max(n.value, 1))()
+        names = (C.c_char_p * max(n.value, 1))()
+        _raise(_capi.lib().gd_ctx_kernel_times(self._h, ms, names, n.value, C.byref(n)))
+        return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
+
     def close(self) -> None:
         if self._h:
             _capi.lib().gd_ctx_destroy(self._h)

@@ -94,6 +94,9 @@ SIGNATURES = {
     "gd_ctx_set_stream": (C.c_int, [_P, _P]),
     "gd_ctx_synchronize": (C.c_int, [_P]),
     "gd_ctx_launch_count": (C.c_int64, [_P]),
+    "gd_ctx_set_timing": (C.c_int, [_P, C.c_int]),
+    "gd_ctx_kernel_times": (C.c_int, [_P, C.POINTER(C.c_float), C.POINTER(C.c_char_p), C.c_int32,
+                                      C.POINTER(C.c_int32)]),
     "gd_model_upload_gbt": (C.c_int, [_P, C.POINTER(ForestView), C.c_double, C.c_double, C.c_int32, C.c_int32,
                                       C.POINTER(_P)]),
     "gd_model_upload_linear": (C.c_int, [_P, _P, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.POINTER(_P)]),

@@ -251,6 +251,23 @@ int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t me
     return GD_OK;
 }
 
+// Timing hook: an event after each launch (the first event precedes them).
+cudaEvent_t timing_event(gd_ctx* ctx, size_t i) {
+    while (ctx->events.size() <= i) {
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreate(&ev) != cudaSuccess) return nullptr;
+        ctx->events.push_back(ev);
+    }
+    return ctx->events[i];
+}
+
+void timing_mark(void* user, const char* name) {
+    gd_ctx* ctx = static_cast<gd_ctx*>(user);
+    cudaEvent_t ev = timing_event(ctx, ctx->marks.size() + 1);
+    if (ev) cudaEventRecord(ev, ctx->stream);
+    ctx->marks.push_back(name);
+}
+
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
               gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t) {
     const bool general = g.rec_of_clock != nullptr;
@@ -307,7 +324,15 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     const size_t bytes = gd::grid_scratch_bytes(p, general);
     const size_t i_scr = s.add(bytes);
     GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
-    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches);
+    gd::LaunchMark mark = nullptr;
+    if (ctx->timing) {
+        ctx->marks.clear();
+        cudaEvent_t ev = timing_event(ctx, 0);
+        if (ev) cudaEventRecord(ev, ctx->stream);
+        mark = timing_mark;
+    }
+    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches, mark,
+                                   ctx);
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");
     return GD_OK;
 }
@@ -359,6 +384,7 @@ int gd_ctx_destroy(gd_ctx* ctx) {
         cudaStreamSynchronize(ctx->own);
         cudaStreamDestroy(ctx->own);
     }
+    for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     delete ctx;
     return GD_OK;
 }
@@ -377,6 +403,30 @@ int gd_ctx_synchronize(gd_ctx* ctx) {
 }
 
 int64_t gd_ctx_launch_count(const gd_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int gd_ctx_set_timing(gd_ctx* ctx, int on) {
+    if (!ctx) return set_error(GD_ERR_INVALID_ARGUMENT, "null gd_ctx");
+    ctx->timing = on != 0;
+    ctx->marks.clear();
+    return GD_OK;
+}
+
+int gd_ctx_kernel_times(gd_ctx* ctx, float* ms, const char** names, int32_t max, int32_t* n) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if (!n) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_ctx_kernel_times: null n");
+    const int32_t k = static_cast<int32_t>(ctx->marks.size());
+    *n = k;
+    for (int32_t i = 0; i < k && i < max; ++i) {
+        GD_CUDA(cudaEventSynchronize(ctx->events[static_cast<size_t>(i) + 1]), "cudaEventSynchronize");
+        float t = 0.0f;
+        GD_CUDA(cudaEventElapsedTime(&t, ctx->events[static_cast<size_t>(i)], ctx->events[static_cast<size_t>(i) + 1]),
+                "cudaEventElapsedTime");
+        if (ms) ms[i] = t;
+        if (names) names[i] = ctx->marks[static_cast<size_t>(i)];
+    }
+    return GD_OK;
+}
 
 int gd_model_upload_gbt(gd_ctx* ctx, const gd_forest_view* f, double base, double lr, int32_t n_cols, int32_t target,
                         gd_model** out) {

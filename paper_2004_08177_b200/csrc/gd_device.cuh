@@ -106,8 +106,10 @@ int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* 
 // incremented per kernel launched.
 int64_t grid_scratch_per_app(const GridParams& p);
 size_t grid_scratch_bytes(const GridParams& p, bool general);
+// `mark(name)`, if set, is called after each kernel launch (timing hook).
+typedef void (*LaunchMark)(void* user, const char* name);
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
-                       size_t scratch_bytes, int64_t* launches);
+                       size_t scratch_bytes, int64_t* launches, LaunchMark mark = nullptr, void* user = nullptr);
 int launch_select(const SelectParams& p, int sm_count, void* stream);
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
 // Copy `n` packed nodes recoding features sm_col / mem_col as kFeatSm / kFeatMem.

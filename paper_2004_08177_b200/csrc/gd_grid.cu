@@ -1252,7 +1252,7 @@ size_t grid_scratch_bytes(const GridParams& p, bool general) {
 }
 
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
-                       size_t scratch_bytes, int64_t* launches) {
+                       size_t scratch_bytes, int64_t* launches, LaunchMark mark, void* user) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (general) {
         const int cpl = (p.n_clocks + 31) / 32;
@@ -1265,6 +1265,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         else if (cpl <= 12) e = launch_general<12>(p, sm_count, s);
         else e = launch_general<16>(p, sm_count, s);
         if (launches) ++*launches;
+        if (mark) mark(user, "general");
         return e;
     }
     if (p.n_apps == 0) return cudaSuccess;
@@ -1299,6 +1300,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
             grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, p.e_thr,
                                                     p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
+            if (mark) mark(user, "rank");
         }
         WalkParams w{};
         w.wnodes[0] = p.e_wnodes;
@@ -1333,6 +1335,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const int grid = w.n_items < sm_count ? w.n_items : sm_count;
         walk_kern<<<grid, wg.warps * 32, wg.smem, s>>>(w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if (mark) mark(user, "walk");
 
         AccParams a{};
         a.nodes[0] = p.e_nodes;
@@ -1364,6 +1367,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         a.objective = p.objective;
         a.best_effort = p.best_effort;
         if ((e = static_cast<cudaError_t>(launch_acc_cpl(a, sm_count, s))) != cudaSuccess) return e;
+        if (mark) mark(user, "acc");
         if (launches) *launches += 3;
     }
     return cudaSuccess;

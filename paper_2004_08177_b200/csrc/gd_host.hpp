@@ -16,6 +16,10 @@ struct gd_ctx {
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
+    // Measurement hook (gd_ctx_set_timing): events around each grid kernel.
+    bool timing = false;
+    std::vector<cudaEvent_t> events;  // pool, grown on demand
+    std::vector<const char*> marks;   // kernel name per interval of the last call
 };
 
 struct gd_model {
