@@ -7,8 +7,9 @@ Writes profiles/<round>_launches.csv (per-kernel launch list: count, mean
 duration, DRAM bytes, share of GPU time), profiles/<round>_grid_kernel.txt
 (ncu --set full summary, per-source-line and per-opcode breakdown of the grid
 kernel), profiles/<round>_bench.json (both bench arms) and updates
-profiles/ncu_traffic.json (DRAM bytes per grid-kernel launch, read by
-bench.py for roofline.traffic).
+profiles/ncu_traffic.json (DRAM bytes per grid_acc_kernel launch -- the
+dominant kernel -- from the --set full capture, read by bench.py for
+roofline.traffic).
 """
 import collections
 import csv
@@ -27,7 +28,10 @@ def launches(tag, rnd):
     agg = collections.defaultdict(lambda: collections.defaultdict(float))
     cnt = collections.Counter()
     for r in rows:
-        k = r["Kernel Name"]
+        # kernel + grid size: the 10k-app grid launches and the 64-app
+        # latency-stream launches of the same kernel are listed apart
+        k = f'{r["Kernel Name"][:90]} grid{r["Grid Size"].replace(" ", "")}'
+
         agg[k][r["Metric Name"]] += float(r["Metric Value"])
         if r["Metric Name"] == "gpu__time_duration.sum":
             cnt[k] += 1
@@ -38,14 +42,30 @@ def launches(tag, rnd):
                     "dram_write_bytes_per_launch", "share_of_gpu_time"])
         for k, v in sorted(agg.items(), key=lambda kv: -kv[1]["gpu__time_duration.sum"]):
             n = cnt[k]
-            w.writerow([k[:110], n, round(v["gpu__time_duration.sum"] / n / 1e3, 2),
+            w.writerow([k, n, round(v["gpu__time_duration.sum"] / n / 1e3, 2),
                         int(v.get("dram__bytes_read.sum", 0) / n), int(v.get("dram__bytes_write.sum", 0) / n),
                         round(v["gpu__time_duration.sum"] / total, 4)])
-    grid = {k: v for k, v in agg.items() if "grid_partial_kernel" in k}
-    traffic = None
-    for k, v in grid.items():
-        traffic = int((v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) / cnt[k])
-    return traffic
+
+
+def full_traffic(tag):
+    """DRAM read+write bytes of one grid_acc_kernel launch (the dominant kernel)
+    from the ncu --set full capture."""
+    rep = OUT / f"prof_grid_{tag}.ncu-rep"
+    if not rep.exists():
+        return None
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        if "grid_acc_kernel" in r[hdr.index("Kernel Name")]:
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                i = hdr.index(m)
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[i]]
+                tot += float(r[i].replace(",", "")) * scale
+            return int(tot)
+    return None
 
 
 def kernel_summary(tag, rnd):
@@ -53,9 +73,12 @@ def kernel_summary(tag, rnd):
     parts = []
     for cmd in (["python", "scripts/ncu_summary.py", str(rep), "--raw",
                  r"dram__bytes_(read|write)\.sum$|lts__t_bytes\.sum$|l1tex__t_sector_hit_rate\.pct$|"
-                 r"smsp__inst_executed_pipe_fp64|sm__pipe_fp64_cycles_active"],
-                ["python", "scripts/ncu_lines.py", str(rep), "--top", "30"],
-                ["python", "scripts/ncu_sass.py", str(rep), "--top", "0"]):
+                 r"smsp__inst_executed_pipe_fp64|sm__pipe_fp64_cycles_active|"
+                 r"l1tex__data_bank_conflicts_pipe_lsu_mem_shared\.sum$|smsp__pcsamp_warps_issue_stalled_[a-z_]+$"],
+                ["python", "scripts/ncu_lines.py", str(rep), "--top", "30", "--kernel", "acc"],
+                ["python", "scripts/ncu_lines.py", str(rep), "--top", "30", "--kernel", "walk"],
+                ["python", "scripts/ncu_sass.py", str(rep), "--top", "0", "--kernel", "acc"],
+                ["python", "scripts/ncu_sass.py", str(rep), "--top", "0", "--kernel", "walk"]):
         parts.append("$ " + " ".join(cmd[1:]) + "\n" + subprocess.run(cmd, capture_output=True, text=True,
                                                                           cwd=ROOT).stdout)
     (PROF / f"{rnd}_grid_kernel.txt").write_text("\n".join(parts))
@@ -64,7 +87,8 @@ def kernel_summary(tag, rnd):
 def main():
     tag, rnd = sys.argv[1], sys.argv[2]
     PROF.mkdir(exist_ok=True)
-    traffic = launches(tag, rnd)
+    launches(tag, rnd)
+    traffic = full_traffic(tag)
     if (OUT / f"prof_grid_{tag}.ncu-rep").exists():
         kernel_summary(tag, rnd)
     bench = {}
