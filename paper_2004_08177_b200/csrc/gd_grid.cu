@@ -300,6 +300,12 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
     return r;
 }
 
+// Records are written once and read once by the accumulate kernel: stream
+// them past L2 (evict-first) so the models' nodes stay L2-resident.
+__device__ __forceinline__ void store_rec(TreeRec* dst, const TreeRec& r) {
+    __stcs(reinterpret_cast<int4*>(dst), make_int4(static_cast<int>(r.info), r.ref, r.ref2, static_cast<int>(r.pad)));
+}
+
 // A root walk that stopped at a clock node, queued for resolution so the
 // (divergent) residue walks run with full warps.
 struct Job {
@@ -328,7 +334,7 @@ __device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0,
         s.saddr = j.saddr;
         Walk w{j.n, 0, 0};
         load_wnode<kAllSmem>(c, s, w);
-        out[rec_index(j.t, tile0 + j.li, p.n_apps)] = resolve_residue<kAllSmem>(p, c, s, w);
+        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_residue<kAllSmem>(p, c, s, w));
     }
     __syncwarp();
     const int rest = count - take;
@@ -347,7 +353,7 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
                                             int& count, int lane, bool v, const Walk& w, int32_t t, uint32_t saddr,
                                             int li, int model, TreeRec* out, int64_t tile0) {
     const bool job = v && wfeat(w.fc) != kFeatLeaf;
-    if (v && !job) out[rec_index(t, tile0 + li, p.n_apps)] = TreeRec{kRecConst, w.key, 0, 0u};
+    if (v && !job) store_rec(out + rec_index(t, tile0 + li, p.n_apps), TreeRec{kRecConst, w.key, 0, 0u});
     const unsigned m = __ballot_sync(kFull, job);
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, saddr, li};
     count += __popc(m);
