@@ -45,15 +45,54 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true", help="skip nvidia-smi sampling (use under ncu)")
     p.add_argument("--w-clk", type=float, default=None, help="experiment: clock-split weight of the synthetic trees")
+    p.add_argument("--apps", type=int, default=None, help="override the config's app count (large configs)")
     return p.parse_args()
 
 
-def workload_config(name: str, world: int):
+# configs[3] is quoted as one 10M-app batch row-sharded over 1/2/4/8 GPUs
+# (strong scaling); the others fix the apps per GPU (weak scaling).
+STRONG = {"c4"}
+
+
+def workload_config(name: str, world: int, apps=None):
     from paper_2004_08177_b200 import workload as W
 
     cfg = dict(W.CONFIGS[name])
+    if apps:
+        cfg["n_apps"] = int(apps)
+    if name in STRONG:
+        return cfg, -(-cfg["n_apps"] // world), cfg["n_apps"]
     per_rank = cfg["n_apps"]
     return cfg, per_rank, per_rank * world
+
+
+def deadlines_device(me, mt, ptrs, A, C_, F, K, g, opts, dev, seed):
+    """W.deadlines_from_times computed in app chunks on
+    the device, so configs[3]'s 10M x 267 time table is never materialised."""
+    import torch
+
+    import paper_2004_08177_b200 as gd
+
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(0.1, 0.9, size=A)
+    bad = rng.random(size=A) < 0.05
+    idx = np.minimum((q * (C_ - 1)).astype(np.int64), C_ - 1)
+    out = np.empty(A)
+    chunk = max(1, min(A, (1 << 28) // (C_ * 8)))
+    t_tab = torch.empty((chunk, C_), dtype=torch.float64, device=dev)
+    for lo in range(0, A, chunk):
+        n = min(chunk, A - lo)
+        d = dict(ptrs)
+        d["rows"] += lo * F * 8
+        d["cat_t"] += lo * K * 8
+        d["budgets"] += lo * 8
+        d["out"] += lo * 24
+        gd.grid_select_device(me, mt, d, n, C_, F, K, g.sm_col, g.mem_col, opts, t_out=t_tab.data_ptr())
+        srt = torch.sort(t_tab[:n], dim=1).values
+        dl = srt.gather(1, torch.from_numpy(idx[lo:lo + n]).to(dev)[:, None])[:, 0]
+        dl = torch.where(torch.from_numpy(bad[lo:lo + n]).to(dev), srt[:, 0] * 0.5, dl)
+        out[lo:lo + n] = dl.cpu().numpy()
+    return out
 
 
 def make_inputs(cfg, n_total, seed=1234, w_clk=None):
@@ -67,7 +106,8 @@ def config_json(name, cfg, per_rank, world, n_clocks):
     return {"workload": f"BASELINE configs[{ {'c2': 1, 'c3': 2, 'c4': 3, 'c5': 4}.get(name, -1) }] ({name}): "
                         f"{per_rank} synthetic apps/GPU x {n_clocks} {cfg['catalog']} clocks, "
                         f"{cfg['n_trees']}-tree depth-{cfg['depth']} GBT energy + time, full_deadline text/energy",
-            "apps_per_gpu": per_rank, "apps_total": per_rank * world, "clocks": n_clocks,
+            "apps_per_gpu": per_rank, "apps_total": per_rank * world if name not in STRONG else cfg["n_apps"],
+            "clocks": n_clocks,
             "trees_per_model": cfg["n_trees"], "depth": cfg["depth"], "columns": 50,
             "parallelism": f"row-sharded dp{world}",
             "l2": "flushed (512 MiB write) before every timed step", "precision": "exact fp64 (bit-identical)"}
@@ -137,7 +177,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    cfg, per_rank, n_total = workload_config(args.config, world)
+    cfg, per_rank, n_total = workload_config(args.config, world, args.apps)
     sc = make_inputs(cfg, n_total, w_clk=args.w_clk)
     lo, hi = shard.shard_range(n_total, rank, world)
     A = hi - lo
@@ -170,12 +210,8 @@ def run_ours(args, rank, world, local_rank):
         gd.grid_select_device(me, mt, ptrs, A, C_, F, K, g.sm_col, g.mem_col, opts)
 
     # Pre-pass (untimed): predicted times -> per-app deadlines.
-    t_tab = torch.empty((A, C_), dtype=torch.float64, device=dev)
-    gd.grid_select_device(me, mt, ptrs, A, C_, F, K, g.sm_col, g.mem_col, opts, t_out=t_tab.data_ptr())
-    torch.cuda.synchronize(dev)
-    budgets = W.deadlines_from_times(t_tab.cpu().numpy(), seed=77 + rank)
+    budgets = deadlines_device(me, mt, ptrs, A, C_, F, K, g, opts, dev, seed=77 + rank)
     bud_d.copy_(torch.from_numpy(budgets))
-    del t_tab
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     sampler = None
@@ -300,7 +336,8 @@ def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_
         traffic = ncu_traffic(args.config)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong" if args.config in STRONG else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; models random-init in the reference "
                                                            "GbtNode format, rows in the reference 50-column schema)",
             "config": config_json(args.config, cfg, per_rank, world, C_),
@@ -430,7 +467,7 @@ def run_reference(args, rank, world):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
 
-    cfg, per_rank, n_total = workload_config(args.config, world)
+    cfg, per_rank, n_total = workload_config(args.config, world, args.apps)
     if not O.ref_available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libgpudvfs_ref.so not built"}
     sc = make_inputs(cfg, min(n_total, 4096))
@@ -452,7 +489,8 @@ def run_reference(args, rank, world):
     value = n * g.n_clocks / step_s
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "strong" if args.config in STRONG else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_json(args.config, cfg, per_rank, world, g.n_clocks),
         "decisions_per_s": n / step_s,

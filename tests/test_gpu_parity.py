@@ -310,6 +310,30 @@ def test_c2_full_size_properties(ctx):
     assert 0 < ok.sum() < sc.grid.n_apps
 
 
+@pytest.mark.parametrize("shape", ["c3", "c4"])
+def test_deep_config_shapes_sampled_vs_oracle(ctx, shape):
+    # BASELINE configs[2] / configs[3] tree shapes (1000 trees depth 10 on the
+    # 200-clock B200 grid; 2000 trees depth 12 on the 267-clock grid) at a
+    # reduced app count: windowed walks, deep residues; seeded apps against
+    # the oracle bit for bit, the rest through the properties.
+    if shape == "c3":
+        sc, sample = W.make_scenario("c3s", 512, "b200", 1000, 10, seed=4), 6
+    else:
+        sc, sample = W.make_scenario("c4s", 256, "gtx980", 2000, 12, seed=3), 2
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, e, t = gd.grid_select(me, mt, sc.grid, np.ones(sc.grid.n_apps), return_predictions=True)
+    budgets = W.deadlines_from_times(t, seed=6)
+    d1, e1, t1 = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
+    assert np.array_equal(bits(e1), bits(e)) and np.array_equal(bits(t1), bits(t))
+    assert decisions_equal(O.oracle_select(e1, t1, sc.grid.sm, budgets), d1)
+    idx = np.random.default_rng(1).choice(sc.grid.n_apps, sample, replace=False)
+    sub = W.GridInputs(sc.grid.rows[idx], sc.grid.cat_t[idx], sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, W.SM_COL,
+                       W.MEM_COL)
+    want, we, wt = O.oracle_grid(sc.energy, sc.time, sub, budgets[idx])
+    assert np.array_equal(bits(e1[idx]), bits(we)) and np.array_equal(bits(t1[idx]), bits(wt))
+    assert decisions_equal(d1[idx], want)
+
+
 def test_sum_tolerance_statement():
     # The kernels are bit-exact; north_star's 1e-5 relative tolerance is the
     # documented ceiling and is implied by 0-ulp equality above.
