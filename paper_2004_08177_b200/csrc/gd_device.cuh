@@ -28,9 +28,9 @@ static_assert(sizeof(PNode) == 16, "PNode must stay 16 bytes");
 //             thresholds of its feature (-1 for a NaN threshold);
 //   clock:    key = t16 (clamp(floor(thr), 0, 65535));
 //   leaf:     key = packed (grid) index of the leaf;
-//   fc = feat << 16 | child: feat (signed; kFeat* for leaf / clock) in the
-//   high half, the tree-local index of the left child (right = child + 1) in
-//   the low half.  With rank(x) = #{thresholds of the feature < x} (NaN x:
+//   fc = feat << 19 | 8 * child: feat (signed; kFeat* for leaf / clock) in
+//   the top 13 bits, the byte offset of the left child within its tree (right
+//   = +8) in the low 19 bits.  With rank(x) = #{thresholds of the feature < x} (NaN x:
 //   their count), `x <= thr_k  <=>  rank(x) <= k` exactly.
 struct __align__(8) WNode {
     int32_t key;

@@ -141,13 +141,13 @@ struct WalkParams {
 // ---------------------------------------------------------------------------
 
 struct Walk {
-    int32_t n;    // tree-local node index
+    int32_t n;    // byte offset of the current node within its tree (walk nodes)
     int32_t key;
     int32_t fc;   // feat << 16 | child
 };
 
-__device__ __forceinline__ int32_t wfeat(int32_t fc) { return fc >> 16; }
-__device__ __forceinline__ int32_t wchild(int32_t fc) { return fc & 0xffff; }
+__device__ __forceinline__ int32_t wfeat(int32_t fc) { return fc >> 19; }
+__device__ __forceinline__ int32_t wchild(int32_t fc) { return fc & 0x7ffff; }  // byte offset of the left child
 
 // Where one tree's walk nodes live during a stage.
 struct TreeSrc {
@@ -166,12 +166,12 @@ struct WalkCtx {
 
 template <bool kAllSmem>
 __device__ __forceinline__ void load_wnode(const WalkCtx& c, const TreeSrc& s, Walk& w) {
-    if (kAllSmem || static_cast<uint32_t>(w.n) < s.win) {
+    if (kAllSmem || static_cast<uint32_t>(w.n) < 8u * s.win) {
         asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
                      : "=r"(w.key), "=r"(w.fc)
-                     : "r"(s.saddr + static_cast<uint32_t>(w.n) * 8u));
+                     : "r"(s.saddr + static_cast<uint32_t>(w.n)));
     } else {
-        const int2 q = __ldg(reinterpret_cast<const int2*>(c.wnodes + s.wroot + w.n));
+        const int2 q = __ldg(reinterpret_cast<const int2*>(reinterpret_cast<const char*>(c.wnodes + s.wroot) + w.n));
         w.key = q.x;
         w.fc = q.y;
     }
@@ -203,7 +203,7 @@ __device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], c
         any = false;
 #pragma unroll
         for (int h = 0; h < N; ++h) {
-            const int32_t nn = wchild(w[h].fc) + (x[h] <= w[h].key ? 0 : 1);
+            const int32_t nn = wchild(w[h].fc) + (x[h] <= w[h].key ? 0 : 8);
             w[h].n = g[h] ? nn : w[h].n;
             load_wnode<kAllSmem>(c, s[h], w[h]);
             g[h] = g[h] && w[h].fc >= 0;
@@ -230,7 +230,7 @@ __device__ __forceinline__ uint2 test_mk(const Walk& w) {
 
 __device__ __forceinline__ double leaf_value(const WalkCtx& c, const Walk& w) { return __ldg(&c.gnodes[w.key].v); }
 
-__device__ __forceinline__ Walk child_walk(const Walk& w, int side) { return Walk{wchild(w.fc) + side, 0, 0}; }
+__device__ __forceinline__ Walk child_walk(const Walk& w, int side) { return Walk{wchild(w.fc) + 8 * side, 0, 0}; }
 
 // Resolve a tree whose root walk stopped at clock node `w` into its record:
 // one test between two leaves -> SM / MEM; a residue of depth <= 3 -> a
@@ -250,7 +250,7 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
         return r;
     }
     r.info = kRecFull;
-    r.ref = s.groot + w.n;
+    r.ref = s.groot + (w.n >> 3);
     const uint32_t idx = atomicAdd(p.pool_count, 1u);
     if (idx >= p.pool_cap) return r;
     RTRec* q = p.pool + idx;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void store_rec(TreeRec* dst, const TreeRec& r) {
 // A root walk that stopped at a clock node, queued for resolution so the
 // (divergent) residue walks run with full warps.
 struct Job {
-    int32_t n;       // the clock node (tree-local index)
+    int32_t n;       // the clock node (byte offset within the tree)
     int32_t t;       // tree
     uint32_t saddr;  // shared address of the tree's window
     int32_t li;      // app within the tile

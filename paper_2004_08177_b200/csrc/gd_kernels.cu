@@ -168,7 +168,7 @@ __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t 
         WNode w;
         if (x.feat == kFeatLeaf) {
             w.key = static_cast<int32_t>(i);
-            w.fc = static_cast<int32_t>(0xffff0000u);
+            w.fc = static_cast<int32_t>(0xfff80000u);  // feat = kFeatLeaf
         } else {
             const int32_t child = x.aux - root;
             if (x.feat < 0) {
@@ -178,7 +178,7 @@ __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t 
                 const int32_t r = rank_of(thr + o, c, x.v);
                 w.key = (x.v == x.v && r < c) ? r : -1;  // exact match; NaN thresholds never pass
             }
-            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 16) | static_cast<uint32_t>(child));
+            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 19) | (static_cast<uint32_t>(child) * 8u));
         }
         dst[__ldg(wroots + lo) + (i - root)] = w;
     }
