@@ -1192,7 +1192,7 @@ struct WalkGeom {
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
-WalkGeom walk_geom(const GridParams& p) {
+WalkGeom walk_geom(const GridParams& p, int64_t batch_apps) {
     constexpr size_t kLimit = 227 * 1024;
     WalkGeom g{};
     g.win_nodes = static_cast<int>(env_i64("GDVFS_WIN_NODES", 512)) & ~1;
@@ -1201,7 +1201,10 @@ WalkGeom walk_geom(const GridParams& p) {
     if (g.win_nodes < 2) g.win_nodes = 2;
     const int32_t max_pair = (p.e_max_pair_nodes > p.t_max_pair_nodes ? p.e_max_pair_nodes : p.t_max_pair_nodes) + 2;
     const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
-    const int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 8));
+    // Small batches (the configs[4] latency stream): no more app groups than
+    // the batch fills, so the CTAs' work items stay short.
+    int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 8));
+    while (max_groups > 1 && 32LL * (max_groups / 2) >= batch_apps) max_groups /= 2;
     for (int groups = 8; groups >= 1; groups >>= 1) {
         if (groups > max_groups) continue;
         const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(2 * groups) +
@@ -1289,7 +1292,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
     if (e != cudaSuccess) return e;
 
-    const WalkGeom wg = walk_geom(p);
+    const WalkGeom wg = walk_geom(p, B);
     // 16-bit ranks and tree-local child indices bound what the walk handles.
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_tree_nodes + 1) & ~1) <= wg.win_nodes;
