@@ -104,6 +104,9 @@ struct AccParams {
     int32_t n_apps;
     int32_t n_cols, n_cat, n_clocks;
     int32_t mode, objective, best_effort;
+    // Sliced mode (small batches): per-app E/T staging and arrival counters.
+    double* et;          // [n_apps][2][n_clocks]
+    uint32_t* arrive;    // [n_apps], zeroed
 };
 
 struct WalkParams {
@@ -1091,6 +1094,89 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
 }
 
 // ---------------------------------------------------------------------------
+// K2b, sliced (latency mode for small batches, e.g. the configs[4] stream):
+// a warp pair per (app, 32-clock slice), lane l owning clock 32*slice + l
+// (one clock per lane, so every memory-clock test is per lane).  Slices
+// publish E/T to a staging row; the last slice to arrive (threadfence +
+// atomic counter) gathers the app's full row and runs the selection.
+// ---------------------------------------------------------------------------
+template <int CPLF>
+__global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __grid_constant__ AccParams p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = warp >> 1;
+    const int model = warp & 1;
+    const int F = p.n_cols, C = p.n_clocks;
+    unsigned char* wsp = smem + acc_smem_per_warp(F) * warp;
+    const uint32_t ws = smem_addr(wsp);
+    double* row = reinterpret_cast<double*>(wsp + kOffRow);
+    AccModel m;
+    m.nodes = model ? p.nodes[1] : p.nodes[0];
+    m.rec = model ? p.rec[1] : p.rec[0];
+    m.n_trees = model ? p.n_trees[1] : p.n_trees[0];
+    const int S = (C + 31) >> 5;
+    const int64_t units = static_cast<int64_t>(p.n_apps) * S;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * (kAccWarps / 2) + pair; u < units;
+         u += static_cast<int64_t>(gridDim.x) * (kAccWarps / 2)) {
+        const int64_t la = u / S;
+        const int sl = static_cast<int>(u - la * S);
+        const int64_t a = p.a0 + la;
+        const int c = sl * 32 + lane;
+        const unsigned ck[1] = {c < C ? ((static_cast<unsigned>(__ldg(p.sm + c)) << 16) |
+                                         static_cast<unsigned>(__ldg(p.mem + c)))
+                                      : 0u};
+        double acc[1] = {0.0};
+        __syncwarp();
+        const double* src = p.rows + a * F;
+        for (int j = lane; j < F; j += 32) row[j] = __ldg(src + j);
+        __syncwarp();
+        if (model == 1) {
+            for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
+            __syncwarp();
+        }
+        accumulate_model<1>(m, p.pool, la, p.n_apps, row, ws, ck, true, ck[0] & 0xffffu, lane, acc);
+        double* et = p.et + la * 2 * C;
+        if (model == 1) {
+            const double t = finish(p.base[1], p.lr[1], acc[0]);
+            if (c < C) {
+                et[C + c] = t;
+                if (p.t_out) p.t_out[a * C + c] = t;
+            }
+            __threadfence();
+            pair_sync_a(pair);  // both warps of the pair have published their slice
+            pair_sync_b(pair);  // the energy warp has read last_flag
+        } else {
+            const double e = clamp_energy(finish(p.base[0], p.lr[0], acc[0]));
+            if (c < C) {
+                et[c] = e;
+                if (p.e_out) p.e_out[a * C + c] = e;
+            }
+            __threadfence();
+            pair_sync_a(pair);
+            int last = 0;
+            if (lane == 0) last = atomicAdd(p.arrive + la, 1u) == static_cast<unsigned>(S - 1);
+            last = __shfl_sync(kFull, last, 0);
+            pair_sync_b(pair);
+            if (last) {
+                __threadfence();
+                double E[CPLF], T[CPLF];
+                int smv[CPLF], cidx[CPLF];
+                contiguous_cidx<CPLF>(lane, C, cidx);
+#pragma unroll
+                for (int i = 0; i < CPLF; ++i) {
+                    const int cc = cidx[i];
+                    E[i] = cc >= 0 ? __ldcg(et + cc) : 0.0;
+                    T[i] = cc >= 0 ? __ldcg(et + C + cc) : 0.0;
+                    smv[i] = cc >= 0 ? __ldg(p.sm + cc) : 0;
+                }
+                select_epilogue<CPLF>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective,
+                                      p.best_effort, p.out + a);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Rows genuinely differ per clock (nearest-record substitution from several
 // profiled records, scheduler.cpp:341-359): full traversal per candidate.
 // ---------------------------------------------------------------------------
@@ -1174,6 +1260,33 @@ int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
+template <int CPLF>
+int launch_acc_sliced(const AccParams& p, int sm_count, cudaStream_t stream) {
+    const size_t smem = acc_smem_per_warp(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
+    auto kern = grid_acc_sliced_kernel<CPLF>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAccThreads, smem);
+    const int64_t units = static_cast<int64_t>(p.n_apps) * ((p.n_clocks + 31) / 32);
+    const int blocks = grid_blocks(kAccWarps / 2, units, sm_count, per_sm);
+    kern<<<blocks, kAccThreads, smem, stream>>>(p);
+    return cudaGetLastError();
+}
+
+int launch_acc_sliced_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
+    const int cpl = (p.n_clocks + 31) / 32;
+    if (cpl <= 1) return launch_acc_sliced<1>(p, sm_count, s);
+    if (cpl <= 2) return launch_acc_sliced<2>(p, sm_count, s);
+    if (cpl <= 4) return launch_acc_sliced<4>(p, sm_count, s);
+    if (cpl <= 7) return launch_acc_sliced<7>(p, sm_count, s);
+    if (cpl <= 9) return launch_acc_sliced<9>(p, sm_count, s);
+    if (cpl <= 12) return launch_acc_sliced<12>(p, sm_count, s);
+    return launch_acc_sliced<16>(p, sm_count, s);
+}
+
 int launch_acc_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
     const int cpl = (p.n_clocks + 31) / 32;
     if (cpl <= 1) return launch_acc<1>(p, sm_count, s);
@@ -1234,6 +1347,13 @@ int64_t pool_per_app(const GridParams& p) {
     return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 1;
 }
 
+// Latency mode for small batches: one warp pair per (app, 32-clock slice)
+// instead of per app (GDVFS_ACC_SLICED=0/1 forces it).
+bool acc_sliced(int64_t n_apps) {
+    const int64_t f = env_i64("GDVFS_ACC_SLICED", -1);
+    return f >= 0 ? f != 0 : n_apps <= 256;
+}
+
 // Apps per batch: the walk records of one batch stay bounded (and, at the
 // default budget, mostly L2-resident between the two kernels).
 int64_t batch_apps(const GridParams& p) {
@@ -1250,7 +1370,9 @@ int64_t grid_scratch_per_app(const GridParams& p) {
     const int64_t pairs = ((p.e_trees + 1) >> 1) + ((p.t_trees + 1) >> 1);
     const int64_t pool = pool_per_app(p);  // residue tables per app
     const int64_t ranks = (2LL * p.n_cols * 2 + 15) & ~15LL;
-    return pairs * 2 * static_cast<int64_t>(sizeof(TreeRec)) + pool * static_cast<int64_t>(sizeof(RTRec)) + ranks;
+    int64_t bytes = pairs * 2 * static_cast<int64_t>(sizeof(TreeRec)) + pool * static_cast<int64_t>(sizeof(RTRec)) + ranks;
+    if (acc_sliced(p.n_apps)) bytes += 2LL * p.n_clocks * 8 + 16;  // E/T staging + arrival counter
+    return bytes;
 }
 
 size_t grid_scratch_bytes(const GridParams& p, bool general) {
@@ -1288,7 +1410,10 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     TreeRec* rec_t = rec_e + B * pe * 2;
     RTRec* pool = reinterpret_cast<RTRec*>(rec_t + B * pt * 2);
     uint16_t* ranks = reinterpret_cast<uint16_t*>(pool + pool_cap);
-    uint32_t* counts = reinterpret_cast<uint32_t*>(ranks + ((2LL * B * p.n_cols + 7) & ~7LL));
+    const bool sliced = acc_sliced(p.n_apps);
+    double* et = reinterpret_cast<double*>(ranks + ((2LL * B * p.n_cols + 7) & ~7LL));
+    uint32_t* arrive = reinterpret_cast<uint32_t*>(et + (sliced ? 2LL * B * p.n_clocks : 0));
+    uint32_t* counts = arrive + (sliced ? ((B + 3) & ~3LL) : 0);
     cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
     if (e != cudaSuccess) return e;
 
@@ -1375,7 +1500,14 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         a.mode = p.mode;
         a.objective = p.objective;
         a.best_effort = p.best_effort;
-        if ((e = static_cast<cudaError_t>(launch_acc_cpl(a, sm_count, s))) != cudaSuccess) return e;
+        if (sliced) {
+            a.et = et;
+            a.arrive = arrive;
+            if ((e = cudaMemsetAsync(arrive, 0, static_cast<size_t>(n) * 4, s)) != cudaSuccess) return e;
+            if ((e = static_cast<cudaError_t>(launch_acc_sliced_cpl(a, sm_count, s))) != cudaSuccess) return e;
+        } else if ((e = static_cast<cudaError_t>(launch_acc_cpl(a, sm_count, s))) != cudaSuccess) {
+            return e;
+        }
         if (mark) mark(user, "acc");
         if (launches) *launches += 3;
     }

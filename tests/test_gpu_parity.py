@@ -114,8 +114,11 @@ def scenario(name):
                            **kw)
 
 
+@pytest.mark.parametrize("sliced", ["0", "1"])
 @pytest.mark.parametrize("name", list(SCENARIOS))
-def test_k2_grid_predictions_and_decisions_vs_oracle(ctx, name):
+def test_k2_grid_predictions_and_decisions_vs_oracle(ctx, name, sliced, monkeypatch):
+    # both accumulate layouts: warp pair per app, and per (app, clock slice)
+    monkeypatch.setenv("GDVFS_ACC_SLICED", sliced)
     sc = scenario(name)
     me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
     _, e0, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
@@ -139,6 +142,7 @@ KNOBS = {
     "pool_overflow": {"GDVFS_POOL_DIV": "1000000"},
     "ring4": {"GDVFS_WALK_BUFS": "4"},
     "one_group": {"GDVFS_WALK_GROUPS": "1", "GDVFS_WALK_BUFS": "3"},
+    "sliced_acc": {"GDVFS_ACC_SLICED": "1"},
 }
 
 
@@ -154,6 +158,54 @@ def test_k2_internal_paths_vs_oracle(ctx, knob, monkeypatch):
     got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
     assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
     assert decisions_equal(got, want)
+
+
+def _forest_edit(f, **kw):
+    import dataclasses
+    return dataclasses.replace(f, **kw)
+
+
+def test_k2_degenerate_models_and_values(ctx):
+    # Models / rows at the edges of the contract: an ensemble with no trees
+    # (prediction = base), single-leaf trees, NaN thresholds (never taken:
+    # x <= NaN is false), NaN and +/-inf feature values (ranks at the ends),
+    # duplicate thresholds and -0.0 / 0.0 on one feature.
+    sc = W.make_scenario("deg", 80, "gtx980", 24, 6, seed=31, w_clk=0.2)
+    fe, ft = sc.energy, sc.time
+    empty = _forest_edit(fe, tree_offsets=np.zeros(1, np.int64), feature=np.zeros(0, np.int32),
+                         threshold=np.zeros(0), left=np.zeros(0, np.int32), right=np.zeros(0, np.int32),
+                         leaf_value=np.zeros(0))
+    # single-leaf trees appended to the time model
+    n_extra = 5
+    off = np.concatenate([ft.tree_offsets, ft.tree_offsets[-1] + 1 + np.arange(n_extra, dtype=np.int64)])
+    leafy = _forest_edit(ft, tree_offsets=off, feature=np.concatenate([ft.feature, np.full(n_extra, -1, np.int32)]),
+                         threshold=np.concatenate([ft.threshold, np.zeros(n_extra)]),
+                         left=np.concatenate([ft.left, np.full(n_extra, -1, np.int32)]),
+                         right=np.concatenate([ft.right, np.full(n_extra, -1, np.int32)]),
+                         leaf_value=np.concatenate([ft.leaf_value, np.linspace(-1, 1, n_extra)]))
+    thr = fe.threshold.copy()
+    internal = np.nonzero(fe.feature >= 0)[0]
+    rng = np.random.default_rng(3)
+    thr[rng.choice(internal, 20, replace=False)] = np.nan
+    f7 = internal[fe.feature[internal] == 7]
+    thr[f7[::3]] = 0.0
+    thr[f7[1::3]] = -0.0
+    weird = _forest_edit(fe, threshold=thr)
+    rows = sc.grid.rows.copy()
+    rows[::7, 7] = 0.0
+    rows[1::7, 7] = -0.0
+    rows[2::9, 11] = np.nan
+    rows[3::9, 12] = np.inf
+    rows[4::9, 13] = -np.inf
+    g = W.GridInputs(rows, sc.grid.cat_t, sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, W.SM_COL, W.MEM_COL)
+    for e_f, t_f in ((empty, leafy), (weird, leafy), (weird, ft)):
+        me, mt = gd.Model.from_forest(e_f, ctx), gd.Model.from_forest(t_f, ctx)
+        _, _, t0 = O.oracle_grid(e_f, t_f, g, np.ones(g.n_apps))
+        budgets = W.deadlines_from_times(t0, seed=4)
+        want, we, wt = O.oracle_grid(e_f, t_f, g, budgets)
+        got, ge, gt = gd.grid_select(me, mt, g, budgets, return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+        assert decisions_equal(got, want)
 
 
 @pytest.mark.parametrize("n_mem", [1, 4, 31, 32, 40])
