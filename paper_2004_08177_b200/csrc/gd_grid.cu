@@ -1339,10 +1339,10 @@ int64_t env_i64(const char* name, int64_t dflt) {
     return e ? std::atoll(e) : dflt;
 }
 
-// Residue-table capacity per app: 1/8 of the trees (GDVFS_POOL_DIV overrides
+// Residue-table capacity per app: 1/4 of the trees (GDVFS_POOL_DIV overrides
 // the divisor; overflowing tables fall back to FULL records).
 int64_t pool_per_app(const GridParams& p) {
-    int64_t div = env_i64("GDVFS_POOL_DIV", 8);
+    int64_t div = env_i64("GDVFS_POOL_DIV", 4);
     if (div < 1) div = 1;
     return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 1;
 }
