@@ -124,6 +124,7 @@ struct WalkParams {
     int32_t win_nodes;         // per-tree window staged in shared memory (BFS prefix, even)
     int32_t stage_nodes;       // capacity of one stage buffer (walk nodes)
     int32_t n_bufs;            // stage buffers in the ring (2..4)
+    int32_t n_subs;            // warps per 32-app group (1: a warp walks every tree; 2: even / odd)
     TreeRec* rec[2];
     RTRec* pool;
     uint32_t* pool_count;
@@ -519,7 +520,7 @@ template <bool kAllSmem>
 __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant__ WalkParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int TA = p.tile_apps, groups = TA >> 5;
+    const int TA = p.tile_apps, groups = TA >> 5, NSUB = p.n_subs;
     const int group = warp % groups, sub = warp / groups;
     const size_t buf_bytes = static_cast<size_t>(p.stage_nodes) * 8;
     const int NB = p.n_bufs;
@@ -602,19 +603,19 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         const int32_t nt = p.n_trees[ii.model];
         TreeRec* out = p.rec[ii.model];
         int count = 0;
-        // This warp walks trees 2q + sub of four consecutive pairs side by side.
+        // This warp walks the stage's trees t = 2*q0 + sub + NSUB*k, NW side by side.
         const int4* table = tables + buf * kStageTrees;
         constexpr int NW = GD_WALK_NW;
         const int32_t t_last = min(2 * s.q1, nt) - 1;
-        for (int32_t q = s.q0; q < s.q1; q += NW) {
+        for (int32_t t0 = 2 * s.q0 + sub; t0 <= t_last; t0 += NW * NSUB) {
             TreeSrc src[NW];
             int32_t tt[NW];
             bool vv[NW];
             Walk w[NW];
 #pragma unroll
             for (int h = 0; h < NW; ++h) {
-                tt[h] = 2 * (q + h) + sub;
-                vv[h] = valid && q + h < s.q1 && tt[h] < nt;
+                tt[h] = t0 + NSUB * h;
+                vv[h] = valid && tt[h] <= t_last;
                 const int4 e = table[min(tt[h], t_last) - 2 * s.q0];
                 src[h].wroot = e.x;
                 src[h].groot = e.y;
@@ -1301,7 +1302,7 @@ int launch_acc_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
 // Walk-kernel geometry: warps per CTA (two per 32 apps) so the transposed
 // ranks plus two stage buffers of tree windows fit the opt-in shared memory.
 struct WalkGeom {
-    int warps, win_nodes, stage_nodes, n_bufs;
+    int warps, win_nodes, stage_nodes, n_bufs, n_subs;
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
@@ -1316,14 +1317,18 @@ WalkGeom walk_geom(const GridParams& p, int64_t batch_apps) {
     const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
     // Small batches (the configs[4] latency stream): no more app groups than
     // the batch fills, so the CTAs' work items stay short.
-    int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 8));
+    // 16 warps per CTA: 16 groups x 1 warp (512 apps per tile, every warp
+    // walks every tree of a stage) or 8 groups x 2 warps (even / odd trees).
+    g.n_subs = static_cast<int>(env_i64("GDVFS_WALK_SUBS", 1)) == 2 ? 2 : 1;
+    int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 16 / g.n_subs));
+    if (max_groups > 16 / g.n_subs) max_groups = 16 / g.n_subs;
     while (max_groups > 1 && 32LL * (max_groups / 2) >= batch_apps) max_groups /= 2;
-    for (int groups = 8; groups >= 1; groups >>= 1) {
+    for (int groups = 16; groups >= 1; groups >>= 1) {
         if (groups > max_groups) continue;
-        const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(2 * groups) +
+        const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(g.n_subs * groups) +
                              static_cast<size_t>(g.n_bufs) * kStageTrees * 16;
         if (fixed + g.n_bufs * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
-        g.warps = 2 * groups;
+        g.warps = g.n_subs * groups;
         int64_t stage = static_cast<int64_t>((kLimit - fixed) / (8 * g.n_bufs)) & ~1;
         if (stage > 16384) stage = 16384;
         g.stage_nodes = static_cast<int>(stage);
@@ -1450,7 +1455,8 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.ranks = ranks;
         w.n_apps = n;
         w.n_cols = p.n_cols;
-        w.tile_apps = wg.warps * 16;
+        w.tile_apps = wg.warps / wg.n_subs * 32;
+        w.n_subs = wg.n_subs;
         w.win_nodes = wg.win_nodes;
         w.stage_nodes = wg.stage_nodes;
         w.n_bufs = wg.n_bufs;
