@@ -255,7 +255,12 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
     }
     r.info = kRecFull;
     r.ref = s.groot + (w.n >> 3);
-    const uint32_t idx = atomicAdd(p.pool_count, 1u);
+    // Warp-aggregated allocation among the lanes that got here together.
+    const unsigned am = __activemask();
+    const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(p.pool_count, static_cast<uint32_t>(__popc(am)));
+    const uint32_t idx = __shfl_sync(am, base, leader) + __popc(am & ((1u << lane) - 1u));
     if (idx >= p.pool_cap) return r;
     RTRec* q = p.pool + idx;
     const uint2 left = make_uint2(0u, 0u);
@@ -365,10 +370,11 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
     if (count >= 32) run_jobs<kAllSmem>(p, c0, jobs, count, lane, model, out, tile0);
 }
 
-constexpr int kStageTrees = 128;
+constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
+constexpr int kMaxTileApps = 512;  // apps per walk tile (16 groups of 32)
 #ifndef GD_WALK_NW
 #define GD_WALK_NW 4  // independent walks per lane in the root-walk loop
-#endif  // trees per stage (table entries per buffer)
+#endif
 
 // One stage of the CTA's schedule.
 struct Stage {
@@ -579,13 +585,14 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         const int n_here = static_cast<int>(min(static_cast<int64_t>(TA), p.n_apps - tile0));
         if (ii.tile != row_tile || ii.model != row_model) {
             __syncthreads();  // every warp is done with the previous tile's ranks
-            // Stage the tile's ranks transposed: srank[col * TA + app].
-            const int F = p.n_cols;
-            const uint16_t* src = p.ranks + (static_cast<int64_t>(ii.model) * p.n_apps + tile0) * F;
-            for (int i = threadIdx.x; i < n_here * F; i += blockDim.x) {
-                const int app = i / F, col = i - app * F;
-                srank[col * TA + app] = src[i];
-            }
+            // Stage the tile's ranks ([col][app], already in that layout in
+            // global memory: a contiguous, coalesced 16-byte copy).
+            const int64_t tiles = (p.n_apps + TA - 1) / TA;
+            const int4* src = reinterpret_cast<const int4*>(
+                p.ranks + ((static_cast<int64_t>(ii.model) * tiles + ii.tile) * p.n_cols) * TA);
+            int4* dst = reinterpret_cast<int4*>(srank);
+            const int n16 = p.n_cols * TA / 8;
+            for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
             __syncthreads();
             row_tile = ii.tile;
             row_model = ii.model;
@@ -635,21 +642,25 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     }
 }
 
-// Ranks of the batch's rows for both models: ranks[m][la][f] = #{thresholds
-// of model m on feature f that are < x} (NaN: their count); the time model
-// sees the time-encoded categorical columns.
+// Ranks of the batch's rows for both models, laid out as the walk kernel
+// stages them: ranks[m][tile][f][app in tile] (tile = TA apps), value =
+// #{thresholds of model m on feature f that are < x} (NaN: their count); the
+// time model sees the time-encoded categorical columns.  Consecutive threads
+// take consecutive apps of one (m, tile, f), so the stores are coalesced.
 __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* __restrict__ cat_t,
                                  const int32_t* __restrict__ cat_cols, int32_t n_cat, int64_t a0, int32_t n_apps,
-                                 int32_t F, const double* __restrict__ thr_e, const int32_t* __restrict__ off_e,
-                                 const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
-                                 uint16_t* __restrict__ ranks) {
-    const int64_t total = 2LL * n_apps * F;
+                                 int32_t F, int32_t TA, const double* __restrict__ thr_e,
+                                 const int32_t* __restrict__ off_e, const double* __restrict__ thr_t,
+                                 const int32_t* __restrict__ off_t, uint16_t* __restrict__ ranks) {
+    const int64_t tiles = (n_apps + TA - 1) / TA;
+    const int64_t total = 2LL * tiles * F * TA;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int m = static_cast<int>(i / (static_cast<int64_t>(n_apps) * F));
-        const int64_t rem = i - static_cast<int64_t>(m) * n_apps * F;
-        const int64_t la = rem / F;
-        const int f = static_cast<int>(rem - la * F);
+        const int64_t plane = i / TA;  // (m * tiles + tile) * F + f
+        const int64_t la = (plane / F % tiles) * TA + (i - plane * TA);
+        if (la >= n_apps) continue;
+        const int f = static_cast<int>(plane % F);
+        const int m = static_cast<int>(plane / (F * tiles));
         double x = __ldg(rows + (a0 + la) * F + f);
         if (m == 1) {
             for (int k = 0; k < n_cat; ++k)
@@ -1384,7 +1395,9 @@ size_t grid_scratch_bytes(const GridParams& p, bool general) {
     if (general || p.n_apps == 0) return 0;
     const int64_t b = batch_apps(p);
     const int64_t nb = (p.n_apps + b - 1) / b;
-    return static_cast<size_t>(b * grid_scratch_per_app(p)) + static_cast<size_t>(nb) * 4 + 256;
+    // + one tile of rank padding (the rank layout is whole walk tiles)
+    return static_cast<size_t>(b * grid_scratch_per_app(p)) + 4LL * kMaxTileApps * p.n_cols + 16 +
+           static_cast<size_t>(nb) * 4 + 256;
 }
 
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
@@ -1416,7 +1429,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     RTRec* pool = reinterpret_cast<RTRec*>(rec_t + B * pt * 2);
     uint16_t* ranks = reinterpret_cast<uint16_t*>(pool + pool_cap);
     const bool sliced = acc_sliced(p.n_apps);
-    double* et = reinterpret_cast<double*>(ranks + ((2LL * B * p.n_cols + 7) & ~7LL));
+    double* et = reinterpret_cast<double*>(ranks + ((2LL * (B + kMaxTileApps) * p.n_cols + 7) & ~7LL));
     uint32_t* arrive = reinterpret_cast<uint32_t*>(et + (sliced ? 2LL * B * p.n_clocks : 0));
     uint32_t* counts = arrive + (sliced ? ((B + 3) & ~3LL) : 0);
     cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
@@ -1433,11 +1446,12 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const int64_t a0 = b * B;
         const int32_t n = static_cast<int32_t>(p.n_apps - a0 < B ? p.n_apps - a0 : B);
         {
-            const int64_t total = 2LL * n * p.n_cols;
+            const int ta = wg.warps / wg.n_subs * 32;
+            const int64_t total = 2LL * ((n + ta - 1) / ta) * ta * p.n_cols;
             int blocks = static_cast<int>((total + 255) / 256);
             if (blocks > 16 * sm_count) blocks = 16 * sm_count;
-            grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, p.e_thr,
-                                                    p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
+            grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
+                                                    p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             if (mark) mark(user, "rank");
         }
