@@ -1320,28 +1320,33 @@ int64_t env_i64(const char* name, int64_t dflt);
 WalkGeom walk_geom(const GridParams& p, int64_t batch_apps) {
     constexpr size_t kLimit = 227 * 1024;
     WalkGeom g{};
-    g.win_nodes = static_cast<int>(env_i64("GDVFS_WIN_NODES", 512)) & ~1;
     g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
     g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
-    if (g.win_nodes < 2) g.win_nodes = 2;
-    const int32_t max_pair = (p.e_max_pair_nodes > p.t_max_pair_nodes ? p.e_max_pair_nodes : p.t_max_pair_nodes) + 2;
-    const int64_t need_pair = max_pair < 2 * g.win_nodes ? max_pair : 2 * g.win_nodes;
-    // Small batches (the configs[4] latency stream): no more app groups than
-    // the batch fills, so the CTAs' work items stay short.
+    const int32_t max_tree = (p.max_tree_nodes + 1) & ~1;
     // 16 warps per CTA: 16 groups x 1 warp (512 apps per tile, every warp
     // walks every tree of a stage) or 8 groups x 2 warps (even / odd trees).
     g.n_subs = static_cast<int>(env_i64("GDVFS_WALK_SUBS", 1)) == 2 ? 2 : 1;
     int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 16 / g.n_subs));
     if (max_groups > 16 / g.n_subs) max_groups = 16 / g.n_subs;
+    // Small batches (the configs[4] latency stream): no more app groups than
+    // the batch fills, so the CTAs' work items stay short.
     while (max_groups > 1 && 32LL * (max_groups / 2) >= batch_apps) max_groups /= 2;
     for (int groups = 16; groups >= 1; groups >>= 1) {
         if (groups > max_groups) continue;
         const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(g.n_subs * groups) +
                              static_cast<size_t>(g.n_bufs) * kStageTrees * 16;
-        if (fixed + g.n_bufs * 8 * static_cast<size_t>(need_pair) > kLimit) continue;
-        g.warps = g.n_subs * groups;
+        if (fixed + g.n_bufs * 8 * 4 > kLimit) continue;
         int64_t stage = static_cast<int64_t>((kLimit - fixed) / (8 * g.n_bufs)) & ~1;
         if (stage > 16384) stage = 16384;
+        // Tree window: whole trees when a pair fits one stage buffer, else
+        // the largest top-level prefix that does (the rest is read from L2).
+        int64_t win = env_i64("GDVFS_WIN_NODES", 0);
+        if (win <= 0) win = max_tree < stage / 2 ? max_tree : stage / 2;
+        win &= ~1LL;
+        if (win < 2) win = 2;
+        if (2 * win > stage) continue;
+        g.warps = g.n_subs * groups;
+        g.win_nodes = static_cast<int>(win);
         g.stage_nodes = static_cast<int>(stage);
         g.smem = fixed + g.n_bufs * static_cast<size_t>(g.stage_nodes) * 8;
         return g;
