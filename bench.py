@@ -88,11 +88,19 @@ def deadlines_device(me, mt, ptrs, A, C_, F, K, g, opts, dev, seed):
         d["budgets"] += lo * 8
         d["out"] += lo * 24
         gd.grid_select_device(me, mt, d, n, C_, F, K, g.sm_col, g.mem_col, opts, t_out=t_tab.data_ptr())
-        srt = torch.sort(t_tab[:n], dim=1).values
-        dl = srt.gather(1, torch.from_numpy(idx[lo:lo + n]).to(dev)[:, None])[:, 0]
-        dl = torch.where(torch.from_numpy(bad[lo:lo + n]).to(dev), srt[:, 0] * 0.5, dl)
-        out[lo:lo + n] = dl.cpu().numpy()
+        out[lo:lo + n] = deadline_rows(t_tab[:n], idx[lo:lo + n], bad[lo:lo + n])
     return out
+
+
+def deadline_rows(t_rows, idx, bad):
+    """One chunk of W.deadlines_from_times on a (device) tensor of predicted
+    times: the idx-th smallest time per app, half the smallest when `bad`."""
+    import torch
+
+    srt = torch.sort(t_rows, dim=1).values
+    dl = srt.gather(1, torch.from_numpy(idx).to(t_rows.device)[:, None])[:, 0]
+    dl = torch.where(torch.from_numpy(bad).to(t_rows.device), srt[:, 0] * 0.5, dl)
+    return dl.cpu().numpy()
 
 
 def make_inputs(cfg, n_total, seed=1234, w_clk=None):
