@@ -1,3 +1,6 @@
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/micro/dadd_latency scripts/micro/dadd_latency.cu
+// Measured (B200, round 1): 1 warp/SMSP x 1 chain = 21 % of the FP64 pipe (add latency ~9 cycles);
+// 1 warp/SMSP x 4 chains = 86 %, x 9 chains = 92 %; 4 warps/SMSP x 9 chains = 99 %.
 // FP64 add latency / per-warp issue on B200: W warps per SM, K independent
 // __dadd_rn chains per thread.  adds/s per SM vs (W, K) shows how much ILP a
 // warp needs to keep the FP64 pipe busy (the accumulate kernel has CPL = 9).
