@@ -14,22 +14,28 @@
 // leaves or further clock nodes).  The leaf each candidate reaches is exactly
 // predict_row's leaf (models.cpp:71-78), so the ordered sums are bit-exact.
 //
-// Two kernels per app batch:
+// Three kernels per app batch:
 //
-//   K2a grid_walk_kernel  (tree-major, latency / L1 bound)
-//       lanes = 32 apps, every warp of a CTA walks the same trees, so node
-//       loads coalesce at the top levels and hit L1 below; app rows are
-//       staged in shared memory.  Each (app, tree) is resolved into one
-//       16-byte TreeRec: CONST (leaf value), SM / MEM (one clock test between
-//       two leaves), T2 (<= 3 tests, 4 leaves; 48-byte side record) or FULL
-//       (anything deeper: per-clock traversal from the first clock node).
+//   grid_rank_kernel      exact 16-bit ranks of every (app, feature) against
+//       each model's sorted thresholds (x <= thr_k <=> rank(x) <= k), in the
+//       walk kernel's tile layout.
+//   K2a grid_walk_kernel  (tree-major, shared-memory latency bound)
+//       persistent CTAs, tiles of 512 apps (lane = app); trees (8-byte rank-
+//       form WNodes) stream into shared memory by TMA bulk copies through a
+//       full/empty mbarrier ring; every warp walks every staged tree for its
+//       32 apps, four walks in flight per lane.  Walks that stop at a clock
+//       node are resolved from per-warp job queues with full warps.  Each
+//       (app, tree) becomes one 16-byte TreeRec: CONST (leaf), SM / MEM (one
+//       clock test between two leaves), TABLE (balanced depth-2/3 residue,
+//       128-byte side record) or FULL (deeper: per-clock traversal).
 //   K2b grid_acc_kernel   (app-major, FP64-add / issue bound)
-//       a warp PAIR per app (energy warp, time warp), lane l owning the
-//       contiguous catalog clocks l*CPL .. l*CPL+CPL-1 (one in-order
-//       accumulator per clock).  The app's records stream through a
-//       cp.async ring (32 trees per stage, side data one stage behind), and
-//       every record becomes CPL __dadd_rn's in tree order.  The energy warp
-//       then runs the selection epilogue (K3) on the pair's E/T values.
+//       a warp PAIR per app (energy warp, time warp), lane l owning CPL
+//       catalog clocks that share one memory clock (one in-order accumulator
+//       per clock).  Records stream through a cp.async ring (32 trees per
+//       stage; leaf values / tables one stage behind) and become CPL
+//       __dadd_rn's each, in tree order.  The energy warp then runs the
+//       selection epilogue (K3) on the pair's E/T values.  Small batches use
+//       grid_acc_sliced_kernel (a pair per (app, 32-clock slice)).
 //
 // Clock packing.  Each owned clock is one register ck = sm << 16 | mem
 // (1 <= sm, mem <= 65535, validated on the host).  A test `(double)sm <= thr`
