@@ -691,17 +691,27 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
 constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kAccThreads = kAccWarps * 32;
 
-// Per-warp shared region: record ring [3][32] | leaf values [2][32] | right
-// leaf values [2][32] | residue-table slots [2][kSide] | overflow slot | row.
+// Per-warp shared region for a prefetch depth R: record ring [R+1][32] |
+// leaf values [R][32] | right leaf values [R][32] | residue-table slots
+// [R][kSide] | overflow slot | row.  Records are fetched R groups ahead, what
+// they point at R-1 groups ahead.
 constexpr int kSide = 8;
-constexpr int kOffMeta = 0;
-constexpr int kOffVal = kOffMeta + 3 * 32 * 16;
-constexpr int kOffRv = kOffVal + 2 * 32 * 8;
-constexpr int kOffSide = kOffRv + 2 * 32 * 8;
-constexpr int kOffOvf = kOffSide + 2 * kSide * 128;
-constexpr int kOffRow = kOffOvf + 128;
+template <int R>
+struct Ring {
+    static constexpr int kMeta = 0;
+    static constexpr int kVal = kMeta + (R + 1) * 32 * 16;
+    static constexpr int kRv = kVal + R * 32 * 8;
+    static constexpr int kSideOff = kRv + R * 32 * 8;
+    static constexpr int kOvf = kSideOff + R * kSide * 128;
+    static constexpr int kRow = kOvf + 128;
+    __host__ __device__ static constexpr int rs(int g) { return g % (R + 1); }  // record slot
+    __host__ __device__ static constexpr int ss(int g) { return g % R; }        // side slot
+};
+constexpr int kAccRing = 2;     // main kernel (shared memory bound)
+constexpr int kSlicedRing = 4;  // latency mode (few warps: deeper prefetch)
+template <int R>
 __host__ __device__ constexpr size_t acc_smem_per_warp(int n_cols) {
-    return static_cast<size_t>(kOffRow) + static_cast<size_t>((n_cols + 1) & ~1) * 8;
+    return static_cast<size_t>(Ring<R>::kRow) + static_cast<size_t>((n_cols + 1) & ~1) * 8;
 }
 __host__ __device__ constexpr size_t acc_smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
 
@@ -752,36 +762,39 @@ __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nod
 }
 
 // Stage 1 of the ring: the record of tree g*32 + lane.
+template <int R>
 __device__ __forceinline__ void issue_rec(const AccModel& m, int64_t la, int64_t n_apps, int g, int lane,
                                           uint32_t ws) {
     const int32_t t = g * 32 + lane;
     if (t < m.n_trees) {
-        cp_async16(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16), m.rec + rec_index(t, la, n_apps));
+        cp_async16(ws + Ring<R>::kMeta + static_cast<uint32_t>((Ring<R>::rs(g) * 32 + lane) * 16),
+                   m.rec + rec_index(t, la, n_apps));
     }
 }
 
 // Stage 2: what the record points at -- leaf values (CONST, SM / MEM) or the
 // residue table (staged into slot = rank among the group's tables).
+template <int R>
 __device__ __forceinline__ void issue_side(const AccModel& m, const RTRec* __restrict__ pool, int g, int lane,
                                            uint32_t ws) {
     const int32_t t = g * 32 + lane;
     uint32_t kind = kRecFull, ref = 0, ref2 = 0;
     if (t < m.n_trees) {
-        const uint32_t a = ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16);
+        const uint32_t a = ws + Ring<R>::kMeta + static_cast<uint32_t>((Ring<R>::rs(g) * 32 + lane) * 16);
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(kind), "=r"(ref) : "r"(a));
         ref2 = lds_u32(a + 8u);
         kind &= 7u;
     }
     const unsigned tm = __ballot_sync(kFull, kind == kRecTable);
-    const uint32_t vslot = static_cast<uint32_t>(((g & 1) * 32 + lane) * 8);
+    const uint32_t vslot = static_cast<uint32_t>((Ring<R>::ss(g) * 32 + lane) * 8);
     if (kind == kRecConst || kind == kRecSm || kind == kRecMem) {
-        cp_async8(ws + kOffVal + vslot, &m.nodes[static_cast<int32_t>(ref)].v);
-        if (kind != kRecConst) cp_async8(ws + kOffRv + vslot, &m.nodes[static_cast<int32_t>(ref2)].v);
+        cp_async8(ws + Ring<R>::kVal + vslot, &m.nodes[static_cast<int32_t>(ref)].v);
+        if (kind != kRecConst) cp_async8(ws + Ring<R>::kRv + vslot, &m.nodes[static_cast<int32_t>(ref2)].v);
     } else if (kind == kRecTable) {
         const int slot = __popc(tm & ((1u << lane) - 1u));
         if (slot < kSide) {
             const unsigned char* src = reinterpret_cast<const unsigned char*>(pool + ref);
-            const uint32_t dst = ws + kOffSide + static_cast<uint32_t>(((g & 1) * kSide + slot) * 128);
+            const uint32_t dst = ws + Ring<R>::kSideOff + static_cast<uint32_t>((Ring<R>::ss(g) * kSide + slot) * 128);
 #pragma unroll
             for (int k = 0; k < 8; ++k) cp_async16(dst + 16 * k, src + 16 * k);
         }
@@ -817,25 +830,26 @@ struct GroupMasks {
 };
 
 // One non-constant tree j of the group being processed.
-template <int CPL>
+template <int CPL, int R>
 __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __restrict__ pool, uint32_t ws, int g,
                                             int j, const GroupMasks& gm, const double* row,
                                             const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l, int lane,
                                             double (&acc)[CPL]) {
-    const uint32_t slotb = static_cast<uint32_t>(((g % 3) * 32 + j) * 16);
-    const uint32_t vslot = static_cast<uint32_t>(((g & 1) * 32 + j) * 8);
+    using RG = Ring<R>;
+    const uint32_t slotb = static_cast<uint32_t>((RG::rs(g) * 32 + j) * 16);
+    const uint32_t vslot = static_cast<uint32_t>((RG::ss(g) * 32 + j) * 8);
     const unsigned bit = 1u << j;
     if (gm.sm & bit) {
-        const uint32_t info = lds_u32(ws + kOffMeta + slotb);
-        const double lv = lds_f64(ws + kOffVal + vslot);
-        const double rv = lds_f64(ws + kOffRv + vslot);
+        const uint32_t info = lds_u32(ws + RG::kMeta + slotb);
+        const double lv = lds_f64(ws + RG::kVal + vslot);
+        const double rv = lds_f64(ws + RG::kRv + vslot);
         const unsigned key = (info & 0xffff0000u) | 0xffffu;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] <= key ? lv : rv);
     } else if (gm.mem & bit) {
-        const uint32_t info = lds_u32(ws + kOffMeta + slotb);
-        const double lv = lds_f64(ws + kOffVal + vslot);
-        const double rv = lds_f64(ws + kOffRv + vslot);
+        const uint32_t info = lds_u32(ws + RG::kMeta + slotb);
+        const double lv = lds_f64(ws + RG::kVal + vslot);
+        const double rv = lds_f64(ws + RG::kRv + vslot);
         const unsigned key = info >> 16;
         if (mem_uniform) {  // all of this lane's clocks share one memory clock
             add_const<CPL>(acc, mem_l <= key ? lv : rv);
@@ -847,10 +861,10 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
         const int slot = __popc(gm.tab & (bit - 1u));
         uint32_t sb;
         if (slot < kSide) {
-            sb = ws + kOffSide + static_cast<uint32_t>(((g & 1) * kSide + slot) * 128);
+            sb = ws + RG::kSideOff + static_cast<uint32_t>((RG::ss(g) * kSide + slot) * 128);
         } else {  // more tables in this group than staged slots: copy it now
-            const uint32_t ref = lds_u32(ws + kOffMeta + slotb + 4);
-            sb = ws + kOffOvf;
+            const uint32_t ref = lds_u32(ws + RG::kMeta + slotb + 4);
+            sb = ws + RG::kOvf;
             __syncwarp();
             if (lane < 8) {
                 const int4 x = __ldg(reinterpret_cast<const int4*>(pool + ref) + lane);
@@ -863,37 +877,38 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
         if (lds_u32(sb + 56u) == 2u) add_table<CPL, 2>(acc, ck, sb);
         else add_table<CPL, 3>(acc, ck, sb);
     } else {
-        const int32_t ref = static_cast<int32_t>(lds_u32(ws + kOffMeta + slotb + 4));
+        const int32_t ref = static_cast<int32_t>(lds_u32(ws + RG::kMeta + slotb + 4));
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, ref, row, ck[i]));
     }
 }
 
-template <int CPL>
+template <int CPL, int R>
 __device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec* __restrict__ pool, int64_t la,
                                                  int64_t n_apps, const double* row, uint32_t ws,
                                                  const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l,
                                                  int lane, double (&acc)[CPL]) {
+    using RG = Ring<R>;
     const int ng = (m.n_trees + 31) >> 5;
     if (ng == 0) return;
     __syncwarp();
-    issue_rec(m, la, n_apps, 0, lane, ws);
+    // Prologue: records of groups 0 .. R-1, then the side data of 0 .. R-2.
+    for (int j = 0; j < R && j < ng; ++j) issue_rec<R>(m, la, n_apps, j, lane, ws);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    issue_side(m, pool, 0, lane, ws);
-    if (ng > 1) issue_rec(m, la, n_apps, 1, lane, ws);
+    for (int j = 0; j + 1 < R && j < ng; ++j) issue_side<R>(m, pool, j, lane, ws);
     cp_async_commit();
     for (int g = 0; g < ng; ++g) {
         cp_async_wait_all();
         __syncwarp();
-        if (g + 1 < ng) issue_side(m, pool, g + 1, lane, ws);
-        if (g + 2 < ng) issue_rec(m, la, n_apps, g + 2, lane, ws);
+        if (g + R - 1 < ng) issue_side<R>(m, pool, g + R - 1, lane, ws);
+        if (g + R < ng) issue_rec<R>(m, la, n_apps, g + R, lane, ws);
         cp_async_commit();
 
         const int nth = min(32, m.n_trees - g * 32);
-        const uint32_t vals = ws + kOffVal + static_cast<uint32_t>((g & 1) * 32 * 8);
-        const uint32_t kind_l = lane < nth ? (lds_u32(ws + kOffMeta + static_cast<uint32_t>(((g % 3) * 32 + lane) * 16)) & 7u)
+        const uint32_t vals = ws + RG::kVal + static_cast<uint32_t>(RG::ss(g) * 32 * 8);
+        const uint32_t kind_l = lane < nth ? (lds_u32(ws + RG::kMeta + static_cast<uint32_t>((RG::rs(g) * 32 + lane) * 16)) & 7u)
                                            : kRecConst;
         GroupMasks gm;
         gm.nc = __ballot_sync(kFull, kind_l != kRecConst);
@@ -925,7 +940,7 @@ __device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec*
             }
             if (k < r) add_const<CPL>(acc, lds_f64(vals + static_cast<uint32_t>(k * 8)));
             if (r >= nth) break;
-            add_residue<CPL>(m, pool, ws, g, r, gm, row, ck, mem_uniform, mem_l, lane, acc);
+            add_residue<CPL, R>(m, pool, ws, g, r, gm, row, ck, mem_uniform, mem_l, lane, acc);
             rest &= rest - 1u;
             j = r + 1;
         }
@@ -1032,16 +1047,17 @@ __device__ int build_clock_map(const int32_t* __restrict__ mem, int C, int cpl, 
 
 template <int CPL>
 __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCKS)) grid_acc_kernel(const __grid_constant__ AccParams p) {
+    constexpr int RING = kAccRing;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
     const int model = warp & 1;  // 0 energy, 1 time
     const int F = p.n_cols;
-    unsigned char* wsp = smem + acc_smem_per_warp(F) * warp;
+    unsigned char* wsp = smem + acc_smem_per_warp<RING>(F) * warp;
     const uint32_t ws = smem_addr(wsp);
-    double* row = reinterpret_cast<double*>(wsp + kOffRow);
-    double* tbuf = reinterpret_cast<double*>(smem + acc_smem_per_warp(F) * kAccWarps + acc_smem_per_pair(CPL) * pair);
-    int16_t* map = reinterpret_cast<int16_t*>(smem + acc_smem_per_warp(F) * kAccWarps +
+    double* row = reinterpret_cast<double*>(wsp + Ring<RING>::kRow);
+    double* tbuf = reinterpret_cast<double*>(smem + acc_smem_per_warp<RING>(F) * kAccWarps + acc_smem_per_pair(CPL) * pair);
+    int16_t* map = reinterpret_cast<int16_t*>(smem + acc_smem_per_warp<RING>(F) * kAccWarps +
                                               acc_smem_per_pair(CPL) * (kAccWarps / 2));
     int* flag = reinterpret_cast<int*>(map + 32 * CPL);
     if (warp == 0) {
@@ -1079,7 +1095,7 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
             for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
         }
-        accumulate_model<CPL>(m, p.pool, la, p.n_apps, row, ws, ck, mem_uniform, mem_l, lane, acc);
+        accumulate_model<CPL, RING>(m, p.pool, la, p.n_apps, row, ws, ck, mem_uniform, mem_l, lane, acc);
         if (model == 1) {
             pair_sync_a(pair);  // the energy warp is done reading the previous app's times
 #pragma unroll
@@ -1120,14 +1136,15 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
 // ---------------------------------------------------------------------------
 template <int CPLF>
 __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __grid_constant__ AccParams p) {
+    constexpr int RING = kSlicedRing;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
     const int model = warp & 1;
     const int F = p.n_cols, C = p.n_clocks;
-    unsigned char* wsp = smem + acc_smem_per_warp(F) * warp;
+    unsigned char* wsp = smem + acc_smem_per_warp<RING>(F) * warp;
     const uint32_t ws = smem_addr(wsp);
-    double* row = reinterpret_cast<double*>(wsp + kOffRow);
+    double* row = reinterpret_cast<double*>(wsp + Ring<RING>::kRow);
     AccModel m;
     m.nodes = model ? p.nodes[1] : p.nodes[0];
     m.rec = model ? p.rec[1] : p.rec[0];
@@ -1152,7 +1169,7 @@ __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __gr
             for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
         }
-        accumulate_model<1>(m, p.pool, la, p.n_apps, row, ws, ck, true, ck[0] & 0xffffu, lane, acc);
+        accumulate_model<1, RING>(m, p.pool, la, p.n_apps, row, ws, ck, true, ck[0] & 0xffffu, lane, acc);
         double* et = p.et + la * 2 * C;
         if (model == 1) {
             const double t = finish(p.base[1], p.lr[1], acc[0]);
@@ -1264,7 +1281,7 @@ int launch_general(const GridParams& p, int sm_count, cudaStream_t stream) {
 
 template <int CPL>
 int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
-    const size_t smem = acc_smem_per_warp(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
+    const size_t smem = acc_smem_per_warp<kAccRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
                         32 * CPL * sizeof(int16_t) + 16;
     auto kern = grid_acc_kernel<CPL>;
     if (smem > 48 * 1024) {
@@ -1280,7 +1297,7 @@ int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
 
 template <int CPLF>
 int launch_acc_sliced(const AccParams& p, int sm_count, cudaStream_t stream) {
-    const size_t smem = acc_smem_per_warp(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
+    const size_t smem = acc_smem_per_warp<kSlicedRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
     auto kern = grid_acc_sliced_kernel<CPLF>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1323,8 +1340,7 @@ struct WalkGeom {
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
-WalkGeom walk_geom(const GridParams& p, int64_t batch_apps) {
-    constexpr size_t kLimit = 227 * 1024;
+WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 * 1024) {
     WalkGeom g{};
     g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
     g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
@@ -1446,7 +1462,14 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
     if (e != cudaSuccess) return e;
 
-    const WalkGeom wg = walk_geom(p, B);
+    // Small batches: a quarter of the shared memory per CTA (shorter stage
+    // buffers) so several CTAs share an SM and the few work items run in
+    // parallel; fall back to the full budget if a tree pair does not fit.
+    WalkGeom wg = walk_geom(p, B);
+    if (wg.warps > 0 && wg.warps < 16) {
+        const WalkGeom small = walk_geom(p, B, 56 * 1024);
+        if (small.warps > 0) wg = small;
+    }
     // 16-bit ranks and tree-local child indices bound what the walk handles.
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_tree_nodes + 1) & ~1) <= wg.win_nodes;
@@ -1497,7 +1520,10 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         if (splits < 1) splits = 1;
         w.splits = static_cast<int32_t>(splits);
         w.n_items = static_cast<int32_t>(tiles * 2 * splits);
-        const int grid = w.n_items < sm_count ? w.n_items : sm_count;
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_kern, wg.warps * 32, wg.smem);
+        if (per_sm < 1) per_sm = 1;
+        const int grid = w.n_items < sm_count * per_sm ? w.n_items : sm_count * per_sm;
         walk_kern<<<grid, wg.warps * 32, wg.smem, s>>>(w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (mark) mark(user, "walk");
