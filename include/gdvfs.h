@@ -212,6 +212,27 @@ int gd_schedule_edf(const gd_job* jobs, int64_t n_jobs, const double* energy, co
                     const double* exec_time, gd_exec_fn exec_fn, void* exec_user, gd_decision* out,
                     int64_t* order);
 
+/* Selection frontier for budget queries (the remaining_time EDF
+ * loop re-selects each job at a budget known only when it is dequeued).  Per
+ * app: t_sorted[a][k] = the app's predicted times sorted by (T, E, catalog
+ * index); best[a][k] = catalog index of select_text's choice
+ * (scheduler.cpp:62-81, objective per `objective`) among the first k + 1 of
+ * them; first[a] = the best-effort choice (argmin (T, E, index),
+ * scheduler.cpp:215-220), or -2 when the app has a non-finite E or T (query
+ * those by a scan).  A budget b is answered by k = #{t_sorted <= b}: choice
+ * best[a][k-1], none if k == 0.  Host buffers; synchronous. */
+int gd_frontier(gd_ctx* ctx, const double* energy, const double* time, int64_t n_apps, const int32_t* sm_clock,
+                int32_t n_clocks, int32_t objective, double* t_sorted, int32_t* best, int32_t* first);
+
+/* gd_schedule_edf with text-mode selections answered from a frontier
+ * (O(log C) per job instead of O(C)); literal mode and rows flagged
+ * first = -2 fall back to the scan.  Same outputs as gd_schedule_edf. */
+int gd_schedule_edf_frontier(const gd_job* jobs, int64_t n_jobs, const double* energy, const double* time,
+                             const double* t_sorted, const int32_t* best, const int32_t* first,
+                             const int32_t* sm_clock, int32_t n_clocks, int32_t budget_kind,
+                             const gd_select_opts* opts, const double* exec_time, gd_exec_fn exec_fn,
+                             void* exec_user, gd_decision* out, int64_t* order);
+
 /* Measure this device's FP64 add throughput (adds/s) with independent
  * __dadd_rn chains: the peak of the path's binding roofline (in-order FP64
  * leaf sums), measured on the same box as the kernel it bounds. */

@@ -316,11 +316,29 @@ def make_jobs(arrival, deadline, app_rank, app_index) -> np.ndarray:
     return jobs
 
 
+def frontier(energy_table, time_table, sm, objective: str = "energy", ctx: Optional[Context] = None):
+    """Per-app selection frontier on the device (gd_frontier): times sorted
+    by (T, E, index), prefix text-mode best index, best-effort index (-2:
+    non-finite row).  Returns (t_sorted, best, first)."""
+    ctx = ctx or default_context()
+    e, t = _c(energy_table, np.float64), _c(time_table, np.float64)
+    sm = _c(sm, np.int32)
+    a, c = e.shape
+    ts = np.empty((a, c), np.float64)
+    best = np.empty((a, c), np.int32)
+    first = np.empty(a, np.int32)
+    _raise(_capi.lib().gd_frontier(ctx.handle, _ptr(e), _ptr(t), a, _ptr(sm), c,
+                                   {"energy": 0, "power": 1}[objective], _ptr(ts), _ptr(best), _ptr(first)))
+    return ts, best, first
+
+
 def schedule_d_dvfs(jobs: np.ndarray, energy_table, time_table, sm, exec_time,
-                    options: Optional[SchedulerOptions] = None):
+                    options: Optional[SchedulerOptions] = None, front=None):
     """schedule_d_dvfs over per-app E/T tables (from :func:`grid_select`):
-    EDF order, remaining/full budgets, selection per job.  Returns
-    (decisions in processing order, job index of each decision)."""
+    EDF order, remaining/full budgets, selection per job.  With ``front``
+    (the :func:`frontier` of the same tables and objective) text-mode jobs
+    are answered by binary search.  Returns (decisions in processing order,
+    job index of each decision)."""
     options = options or SchedulerOptions()
     jobs = np.ascontiguousarray(jobs, JOB_DTYPE)
     e, t = _c(energy_table, np.float64), _c(time_table, np.float64)
@@ -330,8 +348,16 @@ def schedule_d_dvfs(jobs: np.ndarray, energy_table, time_table, sm, exec_time,
     out = np.zeros(n, DECISION_DTYPE)
     order = np.zeros(n, np.int64)
     opts = options.opts()
-    _raise(_capi.lib().gd_schedule_edf(_ptr(jobs), n, _ptr(e), _ptr(t), _ptr(sm), sm.shape[0], BUDGET[options.budget],
-                                       C.byref(opts), _ptr(ex), _capi.EXEC_FN(), None, _ptr(out), _ptr(order)))
+    if front is None:
+        _raise(_capi.lib().gd_schedule_edf(_ptr(jobs), n, _ptr(e), _ptr(t), _ptr(sm), sm.shape[0],
+                                           BUDGET[options.budget], C.byref(opts), _ptr(ex), _capi.EXEC_FN(), None,
+                                           _ptr(out), _ptr(order)))
+    else:
+        ts, best, first = (_c(front[0], np.float64), _c(front[1], np.int32), _c(front[2], np.int32))
+        _raise(_capi.lib().gd_schedule_edf_frontier(_ptr(jobs), n, _ptr(e), _ptr(t), _ptr(ts), _ptr(best),
+                                                    _ptr(first), _ptr(sm), sm.shape[0], BUDGET[options.budget],
+                                                    C.byref(opts), _ptr(ex), _capi.EXEC_FN(), None, _ptr(out),
+                                                    _ptr(order)))
     return out, order
 
 

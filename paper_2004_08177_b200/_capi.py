@@ -113,6 +113,9 @@ SIGNATURES = {
     "gd_microbench_dadd": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "gd_schedule_edf": (C.c_int, [_P, C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, C.POINTER(SelectOpts), _P,
                                   EXEC_FN, _P, _P, _P]),
+    "gd_frontier": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P]),
+    "gd_schedule_edf_frontier": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
+                                           C.POINTER(SelectOpts), _P, EXEC_FN, _P, _P, _P]),
 }
 
 

@@ -745,6 +745,44 @@ int gd_select(gd_ctx* ctx, const double* energy, const double* time, int64_t n_a
     return GD_OK;
 }
 
+int gd_frontier(gd_ctx* ctx, const double* energy, const double* time, int64_t n_apps, const int32_t* sm_clock,
+                int32_t n_clocks, int32_t objective, double* t_sorted, int32_t* best, int32_t* first) {
+    int rc = activate(ctx);
+    if (rc) return rc;
+    if (n_apps < 0 || n_clocks <= 0 || n_clocks > gd::kMaxClocks ||
+        (objective != GD_OBJECTIVE_ENERGY && objective != GD_OBJECTIVE_POWER) ||
+        (n_apps > 0 && (!energy || !time || !sm_clock || !t_sorted || !best || !first))) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "gd_frontier: bad arguments");
+    }
+    if (n_apps == 0) return GD_OK;
+    const int64_t A = n_apps, C = n_clocks;
+    Scratch s{ctx->stream};
+    const size_t i_e = s.add(static_cast<size_t>(A) * C * sizeof(double));
+    const size_t i_t = s.add(static_cast<size_t>(A) * C * sizeof(double));
+    const size_t i_sm = s.add(static_cast<size_t>(C) * sizeof(int32_t));
+    const size_t i_ts = s.add(static_cast<size_t>(A) * C * sizeof(double));
+    const size_t i_b = s.add(static_cast<size_t>(A) * C * sizeof(int32_t));
+    const size_t i_f = s.add(static_cast<size_t>(A) * sizeof(int32_t));
+    GD_CUDA(s.alloc(), "cudaMallocAsync");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_e), energy, s.pieces[i_e].second, cudaMemcpyHostToDevice, ctx->stream), "H2D E");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_t), time, s.pieces[i_t].second, cudaMemcpyHostToDevice, ctx->stream), "H2D T");
+    GD_CUDA(cudaMemcpyAsync(s.ptr(i_sm), sm_clock, s.pieces[i_sm].second, cudaMemcpyHostToDevice, ctx->stream),
+            "H2D sm");
+    int e = gd::launch_frontier(static_cast<double*>(s.ptr(i_e)), static_cast<double*>(s.ptr(i_t)),
+                                static_cast<int32_t*>(s.ptr(i_sm)), A, n_clocks, objective,
+                                static_cast<double*>(s.ptr(i_ts)), static_cast<int32_t*>(s.ptr(i_b)),
+                                static_cast<int32_t*>(s.ptr(i_f)), ctx->sm_count, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "frontier kernel launch");
+    GD_CUDA(cudaMemcpyAsync(t_sorted, s.ptr(i_ts), s.pieces[i_ts].second, cudaMemcpyDeviceToHost, ctx->stream),
+            "D2H t_sorted");
+    GD_CUDA(cudaMemcpyAsync(best, s.ptr(i_b), s.pieces[i_b].second, cudaMemcpyDeviceToHost, ctx->stream), "D2H best");
+    GD_CUDA(cudaMemcpyAsync(first, s.ptr(i_f), s.pieces[i_f].second, cudaMemcpyDeviceToHost, ctx->stream),
+            "D2H first");
+    GD_CUDA(cudaStreamSynchronize(ctx->stream), "frontier sync");
+    return GD_OK;
+}
+
 int gd_microbench_dadd(gd_ctx* ctx, double* adds_per_second) {
     int rc = activate(ctx);
     if (rc) return rc;

@@ -112,6 +112,10 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
                        size_t scratch_bytes, int64_t* launches, LaunchMark mark = nullptr, void* user = nullptr);
 int launch_select(const SelectParams& p, int sm_count, void* stream);
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
+// Selection frontier (gd_kernels.cu frontier_kernel): sorted times, prefix
+// best catalog index, first (best-effort) index or -2 for non-finite rows.
+int launch_frontier(const double* E, const double* T, const int32_t* sm, int64_t n_apps, int32_t n_clocks,
+                    int32_t objective, double* t_sorted, int32_t* best, int32_t* first, int sm_count, void* stream);
 // Copy `n` packed nodes recoding features sm_col / mem_col as kFeatSm / kFeatMem.
 int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t sm_col, int32_t mem_col, void* stream);
 

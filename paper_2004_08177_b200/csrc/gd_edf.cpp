@@ -77,10 +77,51 @@ void select_one(const double* E, const double* T, const int32_t* sm, int32_t n, 
 
 }  // namespace gdh
 
+namespace {
+
+// Text-mode selection answered from a frontier (gd_frontier): k = #{T <= b}
+// by binary search over the app's sorted times; the prefix argmin at k-1 is
+// select_text's choice, first[] the best-effort one.
+void select_frontier(const double* E, const double* T, const double* ts, const int32_t* best, int32_t first,
+                     const int32_t* sm, int32_t n, double budget, const gd_select_opts& o, gd_decision& out) {
+    if (o.mode != GD_MODE_TEXT || first < 0) {
+        gdh::select_one(E, T, sm, n, budget, o, out);
+        return;
+    }
+    std::memset(&out, 0, sizeof(out));
+    const int32_t k = static_cast<int32_t>(std::upper_bound(ts, ts + n, budget) - ts);
+    int32_t chosen = k > 0 ? best[k - 1] : -1;
+    if (chosen < 0 && o.best_effort) {
+        chosen = first;
+        out.note = GD_NOTE_BEST_EFFORT;
+    }
+    if (chosen >= 0) {
+        out.status = GD_SCHEDULED;
+        out.clock_index = chosen;
+        out.energy_ws = E[chosen];
+        out.time_s = T[chosen];
+    } else {
+        out.status = GD_REJECTED;
+        out.clock_index = -1;
+    }
+}
+
+}  // namespace
+
 extern "C" int gd_schedule_edf(const gd_job* jobs, int64_t n_jobs, const double* energy, const double* time,
                                const int32_t* sm_clock, int32_t n_clocks, int32_t budget_kind,
                                const gd_select_opts* opts, const double* exec_time, gd_exec_fn exec_fn,
                                void* exec_user, gd_decision* out, int64_t* order) {
+    return gd_schedule_edf_frontier(jobs, n_jobs, energy, time, nullptr, nullptr, nullptr, sm_clock, n_clocks,
+                                    budget_kind, opts, exec_time, exec_fn, exec_user, out, order);
+}
+
+extern "C" int gd_schedule_edf_frontier(const gd_job* jobs, int64_t n_jobs, const double* energy, const double* time,
+                                        const double* t_sorted, const int32_t* best, const int32_t* first,
+                                        const int32_t* sm_clock, int32_t n_clocks, int32_t budget_kind,
+                                        const gd_select_opts* opts, const double* exec_time, gd_exec_fn exec_fn,
+                                        void* exec_user, gd_decision* out, int64_t* order) {
+    const bool frontier = t_sorted && best && first;
     if (n_jobs < 0 || n_clocks <= 0 || !opts || !out || !order || (n_jobs > 0 && !jobs)) {
         return gdh::set_error(GD_ERR_INVALID_ARGUMENT, "gd_schedule_edf: invalid arguments");
     }
@@ -137,7 +178,12 @@ extern "C" int gd_schedule_edf(const gd_job* jobs, int64_t n_jobs, const double*
             const double budget =
                 budget_kind == GD_BUDGET_FULL ? job.deadline_s : (job.arrival_s + job.deadline_s) - now;
             const int64_t off = static_cast<int64_t>(job.app_index) * n_clocks;
-            gdh::select_one(energy + off, time + off, sm_clock, n_clocks, budget, *opts, d);
+            if (frontier) {
+                select_frontier(energy + off, time + off, t_sorted + off, best + off, first[job.app_index], sm_clock,
+                                n_clocks, budget, *opts, d);
+            } else {
+                gdh::select_one(energy + off, time + off, sm_clock, n_clocks, budget, *opts, d);
+            }
             if (d.status == GD_SCHEDULED) {
                 now += exec_time ? exec_time[off + d.clock_index] : exec_fn(exec_user, e.job, d.clock_index);
             }

@@ -8,6 +8,8 @@
 //   dadd_probe                         FP64 add-pipe peak for the roofline
 //
 // No tensor cores: tree traversal is not a contraction.
+#include <math_constants.h>
+
 #include "gd_common.cuh"
 
 namespace gd {
@@ -113,6 +115,105 @@ __global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ Sel
         contiguous_cidx<CPL>(lane, p.n_clocks, cidx);
         select_epilogue<CPL>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective, p.best_effort,
                              p.out + a);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Selection frontier (the remaining_time EDF loop's per-job query, SURVEY
+// §8f #2): per app, the candidates sorted by (T, E, catalog index) and the
+// prefix argmin of select_text's key (objective, T, sm, index).  For a budget
+// b the feasible set {T <= b} is a prefix of that order, so the text-mode
+// choice is best[k-1] with k = #{T <= b} (one binary search), and the
+// best-effort choice (argmin (T, E, index), scheduler.cpp:215-220) is the
+// first element.  Apps with a non-finite E or T (outside the contract, where
+// the sequential scan is not a total order) get first = -2: the host scans
+// them instead.  One CTA of kFrontThreads per app, bitonic sort in shared
+// memory, Hillis-Steele scan for the prefix argmin.
+// ---------------------------------------------------------------------------
+constexpr int kFrontThreads = 256;
+
+__device__ __forceinline__ bool sort_less(double ta, double ea, int ia, double tb, double eb, int ib) {
+    if (ta != tb) return ta < tb;
+    if (ea != eb) return ea < eb;
+    return ia < ib;
+}
+
+__global__ void __launch_bounds__(kFrontThreads) frontier_kernel(const double* __restrict__ E,
+                                                                 const double* __restrict__ T,
+                                                                 const int32_t* __restrict__ sm, int64_t n_apps,
+                                                                 int32_t C, int32_t objective, double* t_sorted,
+                                                                 int32_t* best, int32_t* first) {
+    __shared__ double st[kMaxClocks], se[kMaxClocks];
+    __shared__ int si[kMaxClocks], sb[kMaxClocks];
+    __shared__ int bad;
+    int P = 1;
+    while (P < C) P <<= 1;
+    for (int64_t a = blockIdx.x; a < n_apps; a += gridDim.x) {
+        if (threadIdx.x == 0) bad = 0;
+        __syncthreads();
+        for (int k = threadIdx.x; k < P; k += blockDim.x) {
+            if (k < C) {
+                st[k] = __ldg(T + a * C + k);
+                se[k] = __ldg(E + a * C + k);
+                si[k] = k;
+                if (!isfinite(st[k]) || !isfinite(se[k])) bad = 1;
+            } else {
+                st[k] = CUDART_INF;
+                se[k] = CUDART_INF;
+                si[k] = INT_MAX;
+            }
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int k = threadIdx.x; k < P; k += blockDim.x) {
+                    const int l = k ^ stride;
+                    if (l > k) {
+                        const bool up = (k & size) == 0;
+                        const bool lt = sort_less(st[l], se[l], si[l], st[k], se[k], si[k]);
+                        if (lt == up) {
+                            const double t = st[k], e = se[k];
+                            const int i = si[k];
+                            st[k] = st[l];
+                            se[k] = se[l];
+                            si[k] = si[l];
+                            st[l] = t;
+                            se[l] = e;
+                            si[l] = i;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // Prefix argmin of (objective, T, sm, index) over the sorted order.
+        for (int k = threadIdx.x; k < C; k += blockDim.x) sb[k] = k;
+        __syncthreads();
+        for (int d = 1; d < C; d <<= 1) {
+            int nb[2] = {0, 0};
+            int m = 0;
+            for (int k = threadIdx.x; k < C; k += blockDim.x, ++m) {
+                int cur = sb[k];
+                if (k >= d) {
+                    const int o = sb[k - d];
+                    Cand x{objective_value(se[o], st[o], objective), st[o], se[o], __ldg(sm + si[o]), si[o]};
+                    Cand y{objective_value(se[cur], st[cur], objective), st[cur], se[cur], __ldg(sm + si[cur]), si[cur]};
+                    if (text_less(x, y)) cur = o;
+                }
+                if (m < 2) nb[m] = cur;
+            }
+            __syncthreads();
+            m = 0;
+            for (int k = threadIdx.x; k < C; k += blockDim.x, ++m)
+                if (m < 2) sb[k] = nb[m];
+            __syncthreads();
+        }
+        for (int k = threadIdx.x; k < C; k += blockDim.x) {
+            t_sorted[a * C + k] = st[k];
+            best[a * C + k] = si[sb[k]];
+        }
+        if (threadIdx.x == 0) first[a] = bad ? -2 : si[0];
+        __syncthreads();
     }
 }
 
@@ -249,6 +350,15 @@ int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, 
     if (blocks < 1) blocks = 1;
     build_walk_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(grid, n, roots, n_trees, wroots,
                                                                                   thr, thr_off, dst);
+    return cudaGetLastError();
+}
+
+int launch_frontier(const double* E, const double* T, const int32_t* sm, int64_t n_apps, int32_t n_clocks,
+                    int32_t objective, double* t_sorted, int32_t* best, int32_t* first, int sm_count, void* stream) {
+    if (n_clocks > 2 * kFrontThreads) return cudaErrorInvalidValue;  // two slots per thread in the scan
+    const int64_t blocks = n_apps < 8LL * sm_count ? n_apps : 8LL * sm_count;
+    frontier_kernel<<<static_cast<int>(blocks > 0 ? blocks : 1), kFrontThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        E, T, sm, n_apps, n_clocks, objective, t_sorted, best, first);
     return cudaGetLastError();
 }
 

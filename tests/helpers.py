@@ -77,3 +77,25 @@ def tie_tables(rng, n_apps, n_clocks, levels=4):
     E = rng.integers(0, levels, size=(n_apps, n_clocks)).astype(np.float64) * 10.0 + 5.0
     T = rng.integers(0, levels, size=(n_apps, n_clocks)).astype(np.float64) * 0.5 + 1.0
     return E, T
+
+
+def frontier_ref(E, T, sm, objective=0):
+    """Plain restatement of gd_frontier (test reference): per app the
+    candidates sorted by (T, E, index), the prefix argmin of select_text's
+    key (objective, T, sm, index), the best-effort index (-2 if non-finite)."""
+    A, Cn = E.shape
+    ts = np.empty((A, Cn))
+    best = np.empty((A, Cn), np.int32)
+    first = np.empty(A, np.int32)
+    for a in range(A):
+        order = sorted(range(Cn), key=lambda c: (T[a, c], E[a, c], c))
+        ts[a] = T[a, order]
+        cur = None
+        for k, c in enumerate(order):
+            obj = E[a, c] / max(T[a, c], 1e-12) if objective else E[a, c]
+            key = (obj, T[a, c], sm[c], c)
+            if cur is None or key < cur[0]:
+                cur = (key, c)
+            best[a, k] = cur[1]
+        first[a] = order[0] if np.all(np.isfinite(E[a])) and np.all(np.isfinite(T[a])) else -2
+    return ts, best, first

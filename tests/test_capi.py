@@ -158,6 +158,32 @@ def test_edf_ties_match_oracle(seed):
         assert np.array_equal(go, wo)
 
 
+@pytest.mark.parametrize("seed", range(4))
+def test_edf_frontier_queries_match_scan(seed):
+    # gd_schedule_edf_frontier (binary search on the per-app frontier) makes
+    # the same decisions as the O(C) scan for every option combination; the
+    # frontier here is the plain restatement (the GPU test checks the kernel).
+    from helpers import frontier_ref
+    rng = np.random.default_rng(100 + seed)
+    n, A, Cn = 300, 20, 33
+    jobs = np.zeros(n, O.JOB_DTYPE)
+    jobs["arrival_s"] = rng.integers(0, 8, size=n).astype(np.float64)
+    jobs["deadline_s"] = rng.integers(1, 9, size=n).astype(np.float64) * 0.5
+    jobs["app_rank"] = rng.permutation(n)
+    jobs["app_index"] = rng.integers(-1, A, size=n)
+    E = rng.integers(0, 4, size=(A, Cn)).astype(np.float64) + 1.0
+    T = rng.integers(1, 6, size=(A, Cn)).astype(np.float64) * 0.25
+    E[3, 4] = np.nan  # a non-finite row falls back to the scan
+    X = T * rng.uniform(0.5, 1.5, size=T.shape)
+    sm = np.sort(rng.integers(300, 2000, size=Cn)).astype(np.int32)  # duplicate sm values allowed
+    for mode, budget, obj, be in itertools.product((0, 1), repeat=4):
+        opts = gd.SchedulerOptions(mode=["text", "literal"][mode], budget=["remaining", "full"][budget],
+                                   objective=["energy", "power"][obj], best_effort_fallback=bool(be))
+        want, wo = gd.schedule_d_dvfs(jobs, E, T, sm, X, opts)
+        got, go = gd.schedule_d_dvfs(jobs, E, T, sm, X, opts, front=frontier_ref(E, T, sm, obj))
+        assert decisions_equal(got, want) and np.array_equal(go, wo), (mode, budget, obj, be)
+
+
 def test_edf_empty_workload():
     out, order = gd.schedule_d_dvfs(np.zeros(0, O.JOB_DTYPE), np.zeros((0, 3)), np.zeros((0, 3)),
                                     np.array([1, 2, 3], np.int32), np.zeros((0, 3)))

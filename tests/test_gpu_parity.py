@@ -328,6 +328,35 @@ def test_k3_tie_breaks_vs_oracle(ctx, n_clocks):
         assert decisions_equal(got, want), combo
 
 
+@pytest.mark.parametrize("n_clocks", [1, 2, 33, 62, 267, 512])
+def test_frontier_kernel_vs_reference(ctx, n_clocks):
+    from helpers import frontier_ref
+    rng = np.random.default_rng(n_clocks)
+    A = 40
+    E, T = tie_tables(rng, A, n_clocks)
+    E[5, 0] = np.inf
+    sm = np.sort(rng.integers(100, 2000, size=n_clocks)).astype(np.int32)
+    for obj in ("energy", "power"):
+        ts, best, first = gd.frontier(E, T, sm, obj, ctx=ctx)
+        wts, wbest, wfirst = frontier_ref(E, T, sm, int(obj == "power"))
+        assert np.array_equal(bits(ts), bits(wts)) and np.array_equal(first, wfirst)
+        ok = wfirst >= 0  # rows flagged non-finite are answered by a scan; their best[] is not used
+        assert np.array_equal(best[ok], wbest[ok])
+
+
+def test_remaining_time_edf_with_frontier_c1_golden(ctx):
+    # The reference's default mode (remaining_time, text) answered from the
+    # GPU frontier == the reference's schedule_d_dvfs decisions.
+    s = c1_small()
+    for tag in ("0000", "0010", "0001", "0011"):
+        mode, budget, obj, be = (int(c) for c in tag)
+        front = gd.frontier(s["pred_energy"], s["pred_time"], s["sm"], ["energy", "power"][obj], ctx=ctx)
+        got, order = gd.schedule_d_dvfs(s["jobs"], s["pred_energy"], s["pred_time"], s["sm"], s["exec"],
+                                        opts_of(mode, budget, obj, be), front=front)
+        want, want_order = c1_combo(s, tag)
+        assert decisions_equal(got, want) and np.array_equal(order, want_order), tag
+
+
 def test_spec_examples_gpu(ctx):
     E, T = np.array([[100.0, 150.0]] * 3), np.array([[10.0, 5.0]] * 3)
     got = gd.select(E, T, np.array([500, 1000], np.int32), np.array([8.0, 12.0, 3.0]), ctx=ctx)
