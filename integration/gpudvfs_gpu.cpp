@@ -363,21 +363,11 @@ std::vector<sched::ScheduleDecision> schedule_d_dvfs(const Workload& workload, c
     t_exec = &exec;
     t_jobs = &workload.jobs;
     t_catalog = &catalog;
-    // Text mode: each job is answered from its GPU selection frontier (binary
-    // search at the job's budget) instead of a scan of all C clocks.
-    std::vector<double> ts;
-    std::vector<int32_t> best, first;
-    if (o.mode == GD_MODE_TEXT && n > 0) {
-        ts.resize(static_cast<std::size_t>(n) * C);
-        best.resize(static_cast<std::size_t>(n) * C);
-        first.resize(static_cast<std::size_t>(n));
-        check(gd_frontier(context(), E.data(), T.data(), n, sm.data(), C, o.objective, ts.data(), best.data(),
-                          first.data()));
-    }
-    check(gd_schedule_edf_frontier(jobs.data(), n, E.data(), T.data(), ts.empty() ? nullptr : ts.data(),
-                                   best.empty() ? nullptr : best.data(), first.empty() ? nullptr : first.data(),
-                                   sm.data(), C, budget, &o, nullptr, exec_trampoline, nullptr, dec.data(),
-                                   order.data()));
+    // The per-job tables live on the host here, so the O(C) scan beats
+    // shipping them to the GPU for a frontier (gd_frontier pays off when the
+    // tables are device-resident; scripts/edf_scale.py).
+    check(gd_schedule_edf(jobs.data(), n, E.data(), T.data(), sm.data(), C, budget, &o, nullptr, exec_trampoline,
+                          nullptr, dec.data(), order.data()));
     std::vector<sched::ScheduleDecision> out;
     out.reserve(static_cast<std::size_t>(n));
     for (int64_t k = 0; k < n; ++k) {
