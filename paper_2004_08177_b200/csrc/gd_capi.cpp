@@ -43,6 +43,8 @@ using gdh::set_error;
 
 namespace {
 
+constexpr size_t kStageLimit = 256 << 10;  // host-buffer calls whose inputs fit are staged
+
 // One stream-ordered scratch allocation carved into aligned pieces.
 struct Scratch {
     cudaStream_t stream;
@@ -261,6 +263,12 @@ cudaEvent_t timing_event(gd_ctx* ctx, size_t i) {
     return ctx->events[i];
 }
 
+void timing_begin(gd_ctx* ctx) {
+    ctx->marks.clear();
+    cudaEvent_t ev = timing_event(ctx, 0);
+    if (ev) cudaEventRecord(ev, ctx->stream);
+}
+
 void timing_mark(void* user, const char* name) {
     gd_ctx* ctx = static_cast<gd_ctx*>(user);
     cudaEvent_t ev = timing_event(ctx, ctx->marks.size() + 1);
@@ -268,8 +276,10 @@ void timing_mark(void* user, const char* name) {
     ctx->marks.push_back(name);
 }
 
+// begin_timing: false when the caller already opened the timing interval list
+// (the host-buffer path marks its copies around the kernels).
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
-              gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t) {
+              gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t, bool begin_timing = true) {
     const bool general = g.rec_of_clock != nullptr;
     if (!general) {
         int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col);
@@ -326,9 +336,7 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
     gd::LaunchMark mark = nullptr;
     if (ctx->timing) {
-        ctx->marks.clear();
-        cudaEvent_t ev = timing_event(ctx, 0);
-        if (ev) cudaEventRecord(ev, ctx->stream);
+        if (begin_timing) timing_begin(ctx);
         mark = timing_mark;
     }
     int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches, mark,
@@ -385,6 +393,11 @@ int gd_ctx_destroy(gd_ctx* ctx) {
         cudaStreamDestroy(ctx->own);
     }
     for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
+    if (ctx->stage_ev) {
+        cudaEventSynchronize(ctx->stage_ev);
+        cudaEventDestroy(ctx->stage_ev);
+    }
+    if (ctx->stage) cudaFreeHost(ctx->stage);
     delete ctx;
     return GD_OK;
 }
@@ -658,17 +671,37 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     const size_t i_t = s.add(t_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
     const size_t i_rt = s.add(g->rec_of_clock ? static_cast<size_t>(R) * g->n_cols * sizeof(double) : 0);
     GD_CUDA(s.alloc(), "cudaMallocAsync");
-    auto h2d = [&](size_t i, const void* src) -> cudaError_t {
-        if (!s.pieces[i].second) return cudaSuccess;
-        return cudaMemcpyAsync(s.ptr(i), src, s.pieces[i].second, cudaMemcpyHostToDevice, ctx->stream);
-    };
-    GD_CUDA(h2d(i_rows, g->rows), "H2D rows");
-    GD_CUDA(h2d(i_cat, g->cat_t), "H2D cat_t");
-    GD_CUDA(h2d(i_catc, g->cat_cols), "H2D cat_cols");
-    GD_CUDA(h2d(i_rec, g->rec_of_clock), "H2D rec_of_clock");
-    GD_CUDA(h2d(i_sm, g->sm_clock), "H2D sm");
-    GD_CUDA(h2d(i_mem, g->mem_clock), "H2D mem");
-    GD_CUDA(h2d(i_bud, g->budgets), "H2D budgets");
+    if (ctx->timing) timing_begin(ctx);
+    // Inputs occupy the scratch prefix [0, in_end).  Small calls (the online
+    // stream's 64-job batches) pack them into pinned staging with the same
+    // offsets and move them in ONE copy: per-copy latency, not bandwidth,
+    // bounds them.  Large calls copy each array straight from the caller.
+    const size_t in_end = s.pieces[i_bud].first + s.pieces[i_bud].second;
+    const std::pair<size_t, const void*> inputs[] = {{i_rows, g->rows},        {i_cat, g->cat_t},
+                                                     {i_catc, g->cat_cols},    {i_rec, g->rec_of_clock},
+                                                     {i_sm, g->sm_clock},      {i_mem, g->mem_clock},
+                                                     {i_bud, g->budgets}};
+    if (in_end <= kStageLimit) {
+        if (!ctx->stage_ev) GD_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming), "stage event");
+        GD_CUDA(cudaEventSynchronize(ctx->stage_ev), "stage reuse");
+        if (!ctx->stage) {
+            GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage), kStageLimit, cudaHostAllocDefault),
+                    "cudaHostAlloc(stage)");
+            ctx->stage_bytes = kStageLimit;
+        }
+        for (const auto& in : inputs) {
+            if (s.pieces[in.first].second) std::memcpy(ctx->stage + s.pieces[in.first].first, in.second, s.pieces[in.first].second);
+        }
+        GD_CUDA(cudaMemcpyAsync(s.base, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream), "H2D staged inputs");
+        GD_CUDA(cudaEventRecord(ctx->stage_ev, ctx->stream), "stage event record");
+    } else {
+        for (const auto& in : inputs) {
+            if (!s.pieces[in.first].second) continue;
+            GD_CUDA(cudaMemcpyAsync(s.ptr(in.first), in.second, s.pieces[in.first].second, cudaMemcpyHostToDevice,
+                                    ctx->stream),
+                    "H2D grid input");
+        }
+    }
     gd_grid dg = *g;
     dg.rows = static_cast<double*>(s.ptr(i_rows));
     dg.cat_t = static_cast<double*>(s.ptr(i_cat));
@@ -677,6 +710,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     dg.sm_clock = static_cast<int32_t*>(s.ptr(i_sm));
     dg.mem_clock = static_cast<int32_t*>(s.ptr(i_mem));
     dg.budgets = static_cast<double*>(s.ptr(i_bud));
+    if (ctx->timing) timing_mark(ctx, "h2d");
     const double* rows_t = nullptr;
     if (g->rec_of_clock) {
         rows_t = static_cast<double*>(s.ptr(i_rt));
@@ -686,7 +720,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
         if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
     }
     rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
-                   static_cast<double*>(s.ptr(i_t)), rows_t);
+                   static_cast<double*>(s.ptr(i_t)), rows_t, false);
     if (rc) return rc;
     GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_out), static_cast<size_t>(A) * sizeof(gd_decision), cudaMemcpyDeviceToHost,
                             ctx->stream),
@@ -701,6 +735,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
                                 ctx->stream),
                 "D2H time");
     }
+    if (ctx->timing) timing_mark(ctx, "d2h");
     GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
     return GD_OK;
 }

@@ -691,27 +691,40 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
 constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kAccThreads = kAccWarps * 32;
 
-// Per-warp shared region for a prefetch depth R: record ring [R+1][32] |
-// leaf values [R][32] | right leaf values [R][32] | residue-table slots
-// [R][kSide] | overflow slot | row.  Records are fetched R groups ahead, what
-// they point at R-1 groups ahead.
+// Per-warp shared region of the two-stage prefetch ring: record slots
+// [RR+1][32] | leaf values [RS+1][32] | right leaf values [RS+1][32] |
+// residue-table slots [RS+1][kSide] | overflow slot | row.  Records are
+// fetched RR groups ahead, what they point at RS groups ahead (RS < RR), as
+// one cp.async commit group per iteration; an iteration waits only for the
+// group that carries its own side data and the records the next side fetch
+// reads, so kWait younger groups stay in flight.
 constexpr int kSide = 8;
-template <int R>
-struct Ring {
+template <int RR, int RS>
+struct RingT {
+    static_assert(RS >= 1 && RR > RS, "records must run ahead of the side data");
+    static constexpr int kRecAhead = RR;
+    static constexpr int kSideAhead = RS;
+    static constexpr int kWait = (RS - 1) < (RR - RS - 1) ? (RS - 1) : (RR - RS - 1);
     static constexpr int kMeta = 0;
-    static constexpr int kVal = kMeta + (R + 1) * 32 * 16;
-    static constexpr int kRv = kVal + R * 32 * 8;
-    static constexpr int kSideOff = kRv + R * 32 * 8;
-    static constexpr int kOvf = kSideOff + R * kSide * 128;
+    static constexpr int kVal = kMeta + (RR + 1) * 32 * 16;
+    static constexpr int kRv = kVal + (RS + 1) * 32 * 8;
+    static constexpr int kSideOff = kRv + (RS + 1) * 32 * 8;
+    static constexpr int kOvf = kSideOff + (RS + 1) * kSide * 128;
     static constexpr int kRow = kOvf + 128;
-    __host__ __device__ static constexpr int rs(int g) { return g % (R + 1); }  // record slot
-    __host__ __device__ static constexpr int ss(int g) { return g % R; }        // side slot
+    __host__ __device__ static constexpr int rs(int g) { return g % (RR + 1); }  // record slot
+    __host__ __device__ static constexpr int ss(int g) { return g % (RS + 1); }  // side slot
 };
-constexpr int kAccRing = 2;     // main kernel (shared memory bound)
-constexpr int kSlicedRing = 4;  // latency mode (few warps: deeper prefetch)
-template <int R>
+#ifndef GD_ACC_RING
+#define GD_ACC_RING 2, 1
+#endif
+#ifndef GD_SLICED_RING
+#define GD_SLICED_RING 8, 4
+#endif
+using AccRing = RingT<GD_ACC_RING>;        // main kernel (shared memory bound)
+using SlicedRing = RingT<GD_SLICED_RING>;  // latency mode (few warps: deep prefetch)
+template <class RG>
 __host__ __device__ constexpr size_t acc_smem_per_warp(int n_cols) {
-    return static_cast<size_t>(Ring<R>::kRow) + static_cast<size_t>((n_cols + 1) & ~1) * 8;
+    return static_cast<size_t>(RG::kRow) + static_cast<size_t>((n_cols + 1) & ~1) * 8;
 }
 __host__ __device__ constexpr size_t acc_smem_per_pair(int cpl) { return 32 * static_cast<size_t>(cpl) * 8; }
 
@@ -723,6 +736,8 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ double lds_f64(uint32_t a) {
     double v;
@@ -762,39 +777,39 @@ __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nod
 }
 
 // Stage 1 of the ring: the record of tree g*32 + lane.
-template <int R>
+template <class RG>
 __device__ __forceinline__ void issue_rec(const AccModel& m, int64_t la, int64_t n_apps, int g, int lane,
                                           uint32_t ws) {
     const int32_t t = g * 32 + lane;
     if (t < m.n_trees) {
-        cp_async16(ws + Ring<R>::kMeta + static_cast<uint32_t>((Ring<R>::rs(g) * 32 + lane) * 16),
+        cp_async16(ws + RG::kMeta + static_cast<uint32_t>((RG::rs(g) * 32 + lane) * 16),
                    m.rec + rec_index(t, la, n_apps));
     }
 }
 
 // Stage 2: what the record points at -- leaf values (CONST, SM / MEM) or the
 // residue table (staged into slot = rank among the group's tables).
-template <int R>
+template <class RG>
 __device__ __forceinline__ void issue_side(const AccModel& m, const RTRec* __restrict__ pool, int g, int lane,
                                            uint32_t ws) {
     const int32_t t = g * 32 + lane;
     uint32_t kind = kRecFull, ref = 0, ref2 = 0;
     if (t < m.n_trees) {
-        const uint32_t a = ws + Ring<R>::kMeta + static_cast<uint32_t>((Ring<R>::rs(g) * 32 + lane) * 16);
+        const uint32_t a = ws + RG::kMeta + static_cast<uint32_t>((RG::rs(g) * 32 + lane) * 16);
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(kind), "=r"(ref) : "r"(a));
         ref2 = lds_u32(a + 8u);
         kind &= 7u;
     }
     const unsigned tm = __ballot_sync(kFull, kind == kRecTable);
-    const uint32_t vslot = static_cast<uint32_t>((Ring<R>::ss(g) * 32 + lane) * 8);
+    const uint32_t vslot = static_cast<uint32_t>((RG::ss(g) * 32 + lane) * 8);
     if (kind == kRecConst || kind == kRecSm || kind == kRecMem) {
-        cp_async8(ws + Ring<R>::kVal + vslot, &m.nodes[static_cast<int32_t>(ref)].v);
-        if (kind != kRecConst) cp_async8(ws + Ring<R>::kRv + vslot, &m.nodes[static_cast<int32_t>(ref2)].v);
+        cp_async8(ws + RG::kVal + vslot, &m.nodes[static_cast<int32_t>(ref)].v);
+        if (kind != kRecConst) cp_async8(ws + RG::kRv + vslot, &m.nodes[static_cast<int32_t>(ref2)].v);
     } else if (kind == kRecTable) {
         const int slot = __popc(tm & ((1u << lane) - 1u));
         if (slot < kSide) {
             const unsigned char* src = reinterpret_cast<const unsigned char*>(pool + ref);
-            const uint32_t dst = ws + Ring<R>::kSideOff + static_cast<uint32_t>((Ring<R>::ss(g) * kSide + slot) * 128);
+            const uint32_t dst = ws + RG::kSideOff + static_cast<uint32_t>((RG::ss(g) * kSide + slot) * 128);
 #pragma unroll
             for (int k = 0; k < 8; ++k) cp_async16(dst + 16 * k, src + 16 * k);
         }
@@ -830,12 +845,11 @@ struct GroupMasks {
 };
 
 // One non-constant tree j of the group being processed.
-template <int CPL, int R>
+template <int CPL, class RG>
 __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __restrict__ pool, uint32_t ws, int g,
                                             int j, const GroupMasks& gm, const double* row,
                                             const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l, int lane,
                                             double (&acc)[CPL]) {
-    using RG = Ring<R>;
     const uint32_t slotb = static_cast<uint32_t>((RG::rs(g) * 32 + j) * 16);
     const uint32_t vslot = static_cast<uint32_t>((RG::ss(g) * 32 + j) * 8);
     const unsigned bit = 1u << j;
@@ -883,27 +897,33 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
     }
 }
 
-template <int CPL, int R>
+template <int CPL, class RG>
 __device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec* __restrict__ pool, int64_t la,
                                                  int64_t n_apps, const double* row, uint32_t ws,
                                                  const unsigned (&ck)[CPL], bool mem_uniform, unsigned mem_l,
                                                  int lane, double (&acc)[CPL]) {
-    using RG = Ring<R>;
     const int ng = (m.n_trees + 31) >> 5;
     if (ng == 0) return;
     __syncwarp();
-    // Prologue: records of groups 0 .. R-1, then the side data of 0 .. R-2.
-    for (int j = 0; j < R && j < ng; ++j) issue_rec<R>(m, la, n_apps, j, lane, ws);
+    constexpr int RR = RG::kRecAhead, RS = RG::kSideAhead;
+    // Prologue: records of groups 0 .. RR-1, then the side data of 0 .. RS-1
+    // (one commit group each, so group g of the loop's wait arithmetic holds
+    // side(g)).
+    for (int j = 0; j < RR && j < ng; ++j) issue_rec<RG>(m, la, n_apps, j, lane, ws);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    for (int j = 0; j + 1 < R && j < ng; ++j) issue_side<R>(m, pool, j, lane, ws);
-    cp_async_commit();
+#pragma unroll
+    for (int j = 0; j < RS; ++j) {
+        if (j < ng) issue_side<RG>(m, pool, j, lane, ws);
+        cp_async_commit();
+    }
     for (int g = 0; g < ng; ++g) {
-        cp_async_wait_all();
+        // Complete: side(g) (group g) and rec(g + RS) (group g + 2RS - RR).
+        cp_async_wait<RG::kWait>();
         __syncwarp();
-        if (g + R - 1 < ng) issue_side<R>(m, pool, g + R - 1, lane, ws);
-        if (g + R < ng) issue_rec<R>(m, la, n_apps, g + R, lane, ws);
+        if (g + RS < ng) issue_side<RG>(m, pool, g + RS, lane, ws);
+        if (g + RR < ng) issue_rec<RG>(m, la, n_apps, g + RR, lane, ws);
         cp_async_commit();
 
         const int nth = min(32, m.n_trees - g * 32);
@@ -940,9 +960,98 @@ __device__ __forceinline__ void accumulate_model(const AccModel& m, const RTRec*
             }
             if (k < r) add_const<CPL>(acc, lds_f64(vals + static_cast<uint32_t>(k * 8)));
             if (r >= nth) break;
-            add_residue<CPL, R>(m, pool, ws, g, r, gm, row, ck, mem_uniform, mem_l, lane, acc);
+            add_residue<CPL, RG>(m, pool, ws, g, r, gm, row, ck, mem_uniform, mem_l, lane, acc);
             rest &= rest - 1u;
             j = r + 1;
+        }
+    }
+}
+
+// One clock per lane (the sliced latency kernel): CONST, SM and MEM records
+// all reduce to one select per tree -- pass ? left : right, with pass forced
+// for CONST -- so the per-tree work is branch-free and the only uniform
+// branch is the rare TABLE / FULL record.  (With one DADD per tree, the run
+// structure of accumulate_model costs more than it saves.)
+template <class RG>
+__device__ __forceinline__ void accumulate_lane(const AccModel& m, const RTRec* __restrict__ pool, int64_t la,
+                                                int64_t n_apps, const double* row, uint32_t ws, unsigned ck, int lane,
+                                                double& acc) {
+    constexpr int RR = RG::kRecAhead, RS = RG::kSideAhead;
+    const int ng = (m.n_trees + 31) >> 5;
+    if (ng == 0) return;
+    const unsigned mem_l = ck & 0xffffu;
+    const unsigned ck1[1] = {ck};
+    double acc1[1];
+    __syncwarp();
+    for (int j = 0; j < RR && j < ng; ++j) issue_rec<RG>(m, la, n_apps, j, lane, ws);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < RS; ++j) {
+        if (j < ng) issue_side<RG>(m, pool, j, lane, ws);
+        cp_async_commit();
+    }
+    for (int g = 0; g < ng; ++g) {
+        cp_async_wait<RG::kWait>();
+        __syncwarp();
+        if (g + RS < ng) issue_side<RG>(m, pool, g + RS, lane, ws);
+        if (g + RR < ng) issue_rec<RG>(m, la, n_apps, g + RR, lane, ws);
+        cp_async_commit();
+
+        const int nth = min(32, m.n_trees - g * 32);
+        const uint32_t meta = ws + RG::kMeta + static_cast<uint32_t>(RG::rs(g) * 32 * 16);
+        const uint32_t vals = ws + RG::kVal + static_cast<uint32_t>(RG::ss(g) * 32 * 8);
+        const uint32_t rvs = ws + RG::kRv + static_cast<uint32_t>(RG::ss(g) * 32 * 8);
+        // Lane t turns tree t's record into a clock test (mask, key):
+        // (ck & mask) <= key picks the left leaf -- CONST (0, 0) always, SM
+        // (0xffff0000, t16 << 16 | 0xffff) iff sm <= t16, MEM (0xffff, t16) iff
+        // mem <= t16 -- written over the record's ref2 / pad words, which the
+        // side fetch has already consumed.
+        uint32_t kind_l = kRecConst;
+        if (lane < nth) {
+            const uint32_t info = lds_u32(meta + static_cast<uint32_t>(lane * 16));
+            kind_l = info & 7u;
+            const uint32_t t16 = info >> 16;
+            if (kind_l <= kRecMem) {
+                const uint32_t mask = kind_l == kRecSm ? 0xffff0000u : (kind_l == kRecMem ? 0xffffu : 0u);
+                const uint32_t key = kind_l == kRecSm ? ((t16 << 16) | 0xffffu) : (kind_l == kRecMem ? t16 : 0u);
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(meta + static_cast<uint32_t>(lane * 16 + 8)),
+                             "r"(mask), "r"(key)
+                             : "memory");
+            }
+        }
+        __syncwarp();
+        GroupMasks gm{0u, 0u, 0u, __ballot_sync(kFull, kind_l == kRecTable)};
+        const unsigned slow = __ballot_sync(kFull, kind_l >= kRecTable);
+        // Blocks of 8 trees: the loads and selects are independent and only
+        // the 8 adds chain (a lone warp per slice has no other latency hiding).
+        for (int j = 0; j < nth; j += 8) {
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {  // slots past nth / slow records: unused values
+                const uint2 mk = lds_u2(meta + static_cast<uint32_t>((j + k) * 16 + 8));
+                const double lv = lds_f64(vals + static_cast<uint32_t>((j + k) * 8));
+                const double rv = lds_f64(rvs + static_cast<uint32_t>((j + k) * 8));
+                v[k] = (ck & mk.x) <= mk.y ? lv : rv;
+            }
+            if (j + 8 <= nth && ((slow >> j) & 0xffu) == 0u) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int t = j + k;
+                    if (t >= nth) break;
+                    if ((slow >> t) & 1u) {
+                        acc1[0] = acc;
+                        add_residue<1, RG>(m, pool, ws, g, t, gm, row, ck1, true, mem_l, lane, acc1);
+                        acc = acc1[0];
+                    } else {
+                        acc = __dadd_rn(acc, v[k]);
+                    }
+                }
+            }
         }
     }
 }
@@ -1047,7 +1156,7 @@ __device__ int build_clock_map(const int32_t* __restrict__ mem, int C, int cpl, 
 
 template <int CPL>
 __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCKS)) grid_acc_kernel(const __grid_constant__ AccParams p) {
-    constexpr int RING = kAccRing;
+    using RING = AccRing;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
@@ -1055,7 +1164,7 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
     const int F = p.n_cols;
     unsigned char* wsp = smem + acc_smem_per_warp<RING>(F) * warp;
     const uint32_t ws = smem_addr(wsp);
-    double* row = reinterpret_cast<double*>(wsp + Ring<RING>::kRow);
+    double* row = reinterpret_cast<double*>(wsp + RING::kRow);
     double* tbuf = reinterpret_cast<double*>(smem + acc_smem_per_warp<RING>(F) * kAccWarps + acc_smem_per_pair(CPL) * pair);
     int16_t* map = reinterpret_cast<int16_t*>(smem + acc_smem_per_warp<RING>(F) * kAccWarps +
                                               acc_smem_per_pair(CPL) * (kAccWarps / 2));
@@ -1136,7 +1245,7 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
 // ---------------------------------------------------------------------------
 template <int CPLF>
 __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __grid_constant__ AccParams p) {
-    constexpr int RING = kSlicedRing;
+    using RING = SlicedRing;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pair = warp >> 1;
@@ -1144,7 +1253,7 @@ __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __gr
     const int F = p.n_cols, C = p.n_clocks;
     unsigned char* wsp = smem + acc_smem_per_warp<RING>(F) * warp;
     const uint32_t ws = smem_addr(wsp);
-    double* row = reinterpret_cast<double*>(wsp + Ring<RING>::kRow);
+    double* row = reinterpret_cast<double*>(wsp + RING::kRow);
     AccModel m;
     m.nodes = model ? p.nodes[1] : p.nodes[0];
     m.rec = model ? p.rec[1] : p.rec[0];
@@ -1169,7 +1278,11 @@ __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __gr
             for (int k = lane; k < p.n_cat; k += 32) row[__ldg(p.cat_cols + k)] = __ldg(p.cat_t + a * p.n_cat + k);
             __syncwarp();
         }
+#ifdef GD_SLICED_RUNS
         accumulate_model<1, RING>(m, p.pool, la, p.n_apps, row, ws, ck, true, ck[0] & 0xffffu, lane, acc);
+#else
+        accumulate_lane<RING>(m, p.pool, la, p.n_apps, row, ws, ck[0], lane, acc[0]);
+#endif
         double* et = p.et + la * 2 * C;
         if (model == 1) {
             const double t = finish(p.base[1], p.lr[1], acc[0]);
@@ -1281,7 +1394,7 @@ int launch_general(const GridParams& p, int sm_count, cudaStream_t stream) {
 
 template <int CPL>
 int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
-    const size_t smem = acc_smem_per_warp<kAccRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
+    const size_t smem = acc_smem_per_warp<AccRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
                         32 * CPL * sizeof(int16_t) + 16;
     auto kern = grid_acc_kernel<CPL>;
     if (smem > 48 * 1024) {
@@ -1297,7 +1410,7 @@ int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
 
 template <int CPLF>
 int launch_acc_sliced(const AccParams& p, int sm_count, cudaStream_t stream) {
-    const size_t smem = acc_smem_per_warp<kSlicedRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
+    const size_t smem = acc_smem_per_warp<SlicedRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
     auto kern = grid_acc_sliced_kernel<CPLF>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -20,6 +20,11 @@ struct gd_ctx {
     bool timing = false;
     std::vector<cudaEvent_t> events;  // pool, grown on demand
     std::vector<const char*> marks;   // kernel name per interval of the last call
+    // Pinned staging for small host-buffer calls (one H2D copy instead of
+    // one per input array); stage_ev guards reuse.
+    char* stage = nullptr;
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev = nullptr;
 };
 
 struct gd_model {
