@@ -653,6 +653,48 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
 // #{thresholds of model m on feature f that are < x} (NaN: their count); the
 // time model sees the time-encoded categorical columns.  Consecutive threads
 // take consecutive apps of one (m, tile, f), so the stores are coalesced.
+// Small batches (latency mode): a warp per rank, 32-ary search -- each round
+// samples the last threshold of 32 equal chunks and keeps the chunk holding
+// the boundary, so ~3 dependent loads replace ~13 of the binary search.
+__global__ void __launch_bounds__(256) grid_rank_warp_kernel(
+    const double* __restrict__ rows, const double* __restrict__ cat_t, const int32_t* __restrict__ cat_cols,
+    int32_t n_cat, int64_t a0, int32_t n_apps, int32_t F, int32_t TA, const double* __restrict__ thr_e,
+    const int32_t* __restrict__ off_e, const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
+    uint16_t* __restrict__ ranks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tiles = (n_apps + TA - 1) / TA;
+    const int64_t total = 2LL * tiles * F * TA;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (i >= total) return;
+    const int64_t plane = i / TA;
+    const int64_t la = (plane / F % tiles) * TA + (i - plane * TA);
+    if (la >= n_apps) return;
+    const int f = static_cast<int>(plane % F);
+    const int m = static_cast<int>(plane / (F * tiles));
+    double x = __ldg(rows + (a0 + la) * F + f);
+    if (m == 1) {
+        for (int k = 0; k < n_cat; ++k)
+            if (__ldg(cat_cols + k) == f) x = __ldg(cat_t + (a0 + la) * n_cat + k);
+    }
+    const double* thr = m ? thr_t : thr_e;
+    const int32_t* off = m ? off_t : off_e;
+    const int32_t o = __ldg(off + f);
+    int lo = 0, hi = __ldg(off + f + 1) - o;  // answer in [lo, hi]
+    if (x != x) lo = hi;
+    while (lo < hi) {
+        const int len = hi - lo;
+        const int step = (len + 31) >> 5;
+        const int last = min(lo + (lane + 1) * step, hi) - 1;  // last index of chunk `lane`
+        const bool in = lo + lane * step < hi;
+        const unsigned below = __ballot_sync(kFull, in && __ldg(thr + o + last) < x);
+        const int c = __popc(below);  // chunks entirely below x (a prefix: thresholds sorted)
+        lo = min(lo + c * step, hi);
+        hi = min(hi, lo + step);
+        if (step == 1) break;  // chunks of one: lo is the count
+    }
+    if (lane == 0) ranks[i] = static_cast<uint16_t>(lo);
+}
+
 __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* __restrict__ cat_t,
                                  const int32_t* __restrict__ cat_cols, int32_t n_cat, int64_t a0, int32_t n_apps,
                                  int32_t F, int32_t TA, const double* __restrict__ thr_e,
@@ -688,6 +730,7 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
 #ifndef GD_ACC_MIN_BLOCKS
 #define GD_ACC_MIN_BLOCKS 6
 #endif
+constexpr int64_t kRankWarpLimit = 1 << 16;  // ranks per batch below which a warp takes each
 constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kAccThreads = kAccWarps * 32;
 
@@ -1025,9 +1068,10 @@ __device__ __forceinline__ void accumulate_lane(const AccModel& m, const RTRec* 
         GroupMasks gm{0u, 0u, 0u, __ballot_sync(kFull, kind_l == kRecTable)};
         const unsigned slow = __ballot_sync(kFull, kind_l >= kRecTable);
         // Blocks of 8 trees: the loads and selects are independent and only
-        // the 8 adds chain (a lone warp per slice has no other latency hiding).
-        for (int j = 0; j < nth; j += 8) {
-            double v[8];
+        // the 8 adds chain (a lone warp per slice has no other latency
+        // hiding).  Software-pipelined: block j's values are formed while
+        // block j-8's adds retire.
+        auto values = [&](int j, double (&v)[8]) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) {  // slots past nth / slow records: unused values
                 const uint2 mk = lds_u2(meta + static_cast<uint32_t>((j + k) * 16 + 8));
@@ -1035,24 +1079,35 @@ __device__ __forceinline__ void accumulate_lane(const AccModel& m, const RTRec* 
                 const double rv = lds_f64(rvs + static_cast<uint32_t>((j + k) * 8));
                 v[k] = (ck & mk.x) <= mk.y ? lv : rv;
             }
-            if (j + 8 <= nth && ((slow >> j) & 0xffu) == 0u) {
+            // TABLE / FULL trees of the block: their value for this lane's
+            // clock, computed into a -0.0-seeded temporary (exact).
+            for (unsigned b = (slow >> j) & 0xffu; b; b &= b - 1u) {
+                const int k = __ffs(b) - 1;
+                acc1[0] = -0.0;
+                add_residue<1, RG>(m, pool, ws, g, j + k, gm, row, ck1, true, mem_l, lane, acc1);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = q == k ? acc1[0] : v[q];
+            }
+        };
+        auto chain = [&](int j, const double (&v)[8]) {
+            if (j + 8 <= nth) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
             } else {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const int t = j + k;
-                    if (t >= nth) break;
-                    if ((slow >> t) & 1u) {
-                        acc1[0] = acc;
-                        add_residue<1, RG>(m, pool, ws, g, t, gm, row, ck1, true, mem_l, lane, acc1);
-                        acc = acc1[0];
-                    } else {
-                        acc = __dadd_rn(acc, v[k]);
-                    }
+                    if (j + k < nth) acc = __dadd_rn(acc, v[k]);
                 }
             }
+        };
+        double va[8];
+        values(0, va);
+        int j = 8;
+        for (; j < nth; j += 8) {
+            chain(j - 8, va);  // independent of the next block's loads and selects
+            values(j, va);
         }
+        chain(j - 8, va);
     }
 }
 
@@ -1595,10 +1650,16 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         {
             const int ta = wg.warps / wg.n_subs * 32;
             const int64_t total = 2LL * ((n + ta - 1) / ta) * ta * p.n_cols;
-            int blocks = static_cast<int>((total + 255) / 256);
-            if (blocks > 16 * sm_count) blocks = 16 * sm_count;
-            grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
-                                                    p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
+            if (total <= kRankWarpLimit) {
+                grid_rank_warp_kernel<<<static_cast<int>((total + 7) / 8), 256, 0, s>>>(
+                    p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
+                    p.t_thr_off, ranks);
+            } else {
+                int blocks = static_cast<int>((total + 255) / 256);
+                if (blocks > 16 * sm_count) blocks = 16 * sm_count;
+                grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
+                                                        p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
+            }
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             if (mark) mark(user, "rank");
         }

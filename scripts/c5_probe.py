@@ -41,3 +41,41 @@ ctx.set_timing(False)
 med = {k: round(float(np.median([s.get(k, 0) for s in spans])) * 1e3, 1) for k in spans[0]}
 print(f"B={B}: wall p50 {np.percentile(lat, 50):.1f} us p99 {np.percentile(lat, 99):.1f} us | timed intervals (us) {med} "
       f"sum {sum(med.values()):.1f}")
+
+# Device-resident inputs: CPU enqueue cost of one grid_select_device call,
+# the synchronous device latency, and the pipelined per-call time.
+dev = torch.device("cuda")
+gw, bw = wins[0]
+keep = dict(rows=torch.from_numpy(gw.rows).to(dev), cat_t=torch.from_numpy(gw.cat_t).to(dev),
+            cat_cols=torch.from_numpy(gw.cat_cols).to(dev), sm=torch.from_numpy(gw.sm.astype(np.int32)).to(dev),
+            mem=torch.from_numpy(gw.mem.astype(np.int32)).to(dev), budgets=torch.from_numpy(bw).to(dev),
+            out=torch.zeros(B * 32, dtype=torch.uint8, device=dev))
+ptrs = {k: v.data_ptr() for k, v in keep.items()}
+C_, F, K = g.n_clocks, g.rows.shape[1], g.cat_t.shape[1]
+ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+
+
+def dev_call():
+    gd.grid_select_device(me, mt, ptrs, B, C_, F, K, g.sm_col, g.mem_col, opts)
+
+
+for _ in range(20):
+    dev_call()
+torch.cuda.synchronize()
+enq, syn = [], []
+for _ in range(200):
+    t0 = time.perf_counter()
+    dev_call()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    enq.append(t1 - t0)
+    syn.append(t2 - t0)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(200):
+    dev_call()
+torch.cuda.synchronize()
+pipe = (time.perf_counter() - t0) / 200
+print(f"B={B} device-resident: enqueue p50 {1e6 * np.median(enq):.1f} us | enqueue+sync p50 {1e6 * np.median(syn):.1f} us"
+      f" | pipelined {1e6 * pipe:.1f} us/call")
