@@ -42,6 +42,9 @@
 // is `ck <= ((clamp(floor(thr), 0, 65535) << 16) | 0xffff)` (unsigned); a test
 // `(double)mem <= thr` is `(ck & 0xffff) <= clamp(floor(thr), 0, 65535)`.
 #include <cstdlib>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "gd_common.cuh"
 
@@ -660,8 +663,11 @@ __global__ void __launch_bounds__(256) grid_rank_warp_kernel(
     const double* __restrict__ rows, const double* __restrict__ cat_t, const int32_t* __restrict__ cat_cols,
     int32_t n_cat, int64_t a0, int32_t n_apps, int32_t F, int32_t TA, const double* __restrict__ thr_e,
     const int32_t* __restrict__ off_e, const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
-    uint16_t* __restrict__ ranks) {
+    uint16_t* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
     const int lane = threadIdx.x & 31;
+    for (int64_t z = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < n_zero;
+         z += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        zero[z] = 0u;
     const int64_t tiles = (n_apps + TA - 1) / TA;
     const int64_t total = 2LL * tiles * F * TA;
     const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -699,7 +705,10 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
                                  const int32_t* __restrict__ cat_cols, int32_t n_cat, int64_t a0, int32_t n_apps,
                                  int32_t F, int32_t TA, const double* __restrict__ thr_e,
                                  const int32_t* __restrict__ off_e, const double* __restrict__ thr_t,
-                                 const int32_t* __restrict__ off_t, uint16_t* __restrict__ ranks) {
+                                 const int32_t* __restrict__ off_t, uint16_t* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
+    for (int64_t z = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < n_zero;
+         z += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        zero[z] = 0u;
     const int64_t tiles = (n_apps + TA - 1) / TA;
     const int64_t total = 2LL * tiles * F * TA;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
@@ -1438,10 +1447,48 @@ __global__ void __launch_bounds__(256) grid_general_kernel(const __grid_constant
     }
 }
 
+// Resident CTAs per SM for (kernel, threads, dynamic smem), raising the
+// kernel's dynamic shared memory limit first when needed.  Cached per device:
+// the attribute call and the occupancy query cost microseconds of host time
+// on every launch otherwise, which the latency stream pays in full.
+int occupancy(const void* fn, int threads, size_t smem) {
+    struct Entry {
+        const void* fn;
+        int device, threads;
+        size_t smem;
+        int per_sm;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    int device = 0;
+    cudaGetDevice(&device);
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        for (const Entry& e : cache) {
+            if (e.fn == fn && e.device == device && e.threads == threads && e.smem == smem) return e.per_sm;
+        }
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    // The limit only ever rises (a cached launch with a larger size must stay
+    // valid after a smaller one was configured).
+    size_t limit = 48 * 1024;
+    for (const Entry& e : cache) {
+        if (e.fn == fn && e.device == device && e.smem > limit) limit = e.smem;
+    }
+    if (smem > limit &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+        return -1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return -1;
+    cache.push_back(Entry{fn, device, threads, smem, per_sm});
+    return per_sm;
+}
+
 template <int CPL>
 int launch_general(const GridParams& p, int sm_count, cudaStream_t stream) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_general_kernel<CPL>, 256, 0);
+    const int per_sm = occupancy(reinterpret_cast<const void*>(grid_general_kernel<CPL>), 256, 0);
+    if (per_sm < 0) return cudaErrorInvalidConfiguration;
     const int blocks = grid_blocks(8, p.n_apps, sm_count, per_sm);
     grid_general_kernel<CPL><<<blocks, 256, 0, stream>>>(p);
     return cudaGetLastError();
@@ -1452,12 +1499,8 @@ int launch_acc(const AccParams& p, int sm_count, cudaStream_t stream) {
     const size_t smem = acc_smem_per_warp<AccRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(CPL) * (kAccWarps / 2) +
                         32 * CPL * sizeof(int16_t) + 16;
     auto kern = grid_acc_kernel<CPL>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAccThreads, smem);
+    const int per_sm = occupancy(reinterpret_cast<const void*>(kern), kAccThreads, smem);
+    if (per_sm < 0) return cudaErrorInvalidConfiguration;
     const int blocks = grid_blocks(kAccWarps / 2, p.n_apps, sm_count, per_sm);
     kern<<<blocks, kAccThreads, smem, stream>>>(p);
     return cudaGetLastError();
@@ -1467,12 +1510,8 @@ template <int CPLF>
 int launch_acc_sliced(const AccParams& p, int sm_count, cudaStream_t stream) {
     const size_t smem = acc_smem_per_warp<SlicedRing>(p.n_cols) * kAccWarps + acc_smem_per_pair(1) * (kAccWarps / 2);
     auto kern = grid_acc_sliced_kernel<CPLF>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAccThreads, smem);
+    const int per_sm = occupancy(reinterpret_cast<const void*>(kern), kAccThreads, smem);
+    if (per_sm < 0) return cudaErrorInvalidConfiguration;
     const int64_t units = static_cast<int64_t>(p.n_apps) * ((p.n_clocks + 31) / 32);
     const int blocks = grid_blocks(kAccWarps / 2, units, sm_count, per_sm);
     kern<<<blocks, kAccThreads, smem, stream>>>(p);
@@ -1627,8 +1666,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     double* et = reinterpret_cast<double*>(ranks + ((2LL * (B + kMaxTileApps) * p.n_cols + 7) & ~7LL));
     uint32_t* arrive = reinterpret_cast<uint32_t*>(et + (sliced ? 2LL * B * p.n_clocks : 0));
     uint32_t* counts = arrive + (sliced ? ((B + 3) & ~3LL) : 0);
-    cudaError_t e = cudaMemsetAsync(counts, 0, static_cast<size_t>(nb) * 4, s);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
 
     // Small batches: a quarter of the shared memory per CTA (shorter stage
     // buffers) so several CTAs share an SM and the few work items run in
@@ -1642,23 +1680,32 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_tree_nodes + 1) & ~1) <= wg.win_nodes;
     auto walk_kern = all_smem ? grid_walk_kernel<true> : grid_walk_kernel<false>;
-    e = cudaFuncSetAttribute(walk_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wg.smem));
-    if (e != cudaSuccess) return e;
+    int walk_per_sm = occupancy(reinterpret_cast<const void*>(walk_kern), wg.warps * 32, wg.smem);
+    if (walk_per_sm < 0) return cudaErrorInvalidConfiguration;
+    if (walk_per_sm < 1) walk_per_sm = 1;
     for (int64_t b = 0; b < nb; ++b) {
         const int64_t a0 = b * B;
         const int32_t n = static_cast<int32_t>(p.n_apps - a0 < B ? p.n_apps - a0 : B);
         {
             const int ta = wg.warps / wg.n_subs * 32;
             const int64_t total = 2LL * ((n + ta - 1) / ta) * ta * p.n_cols;
+            // The rank kernel also zeroes this batch's counters (the walk's
+            // pool count; the sliced accumulate's arrival counters), saving
+            // two memset launches on the latency path.
+            // (Sliced: arrive[] and counts[] are adjacent; earlier batches
+            // are done with theirs, stream order.)
+            uint32_t* zero = sliced ? arrive : counts + b;
+            const int32_t n_zero = sliced ? static_cast<int32_t>(counts + nb - arrive) : 1;
             if (total <= kRankWarpLimit) {
                 grid_rank_warp_kernel<<<static_cast<int>((total + 7) / 8), 256, 0, s>>>(
                     p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
-                    p.t_thr_off, ranks);
+                    p.t_thr_off, ranks, zero, n_zero);
             } else {
                 int blocks = static_cast<int>((total + 255) / 256);
                 if (blocks > 16 * sm_count) blocks = 16 * sm_count;
                 grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
-                                                        p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks);
+                                                        p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks, zero,
+                                                        n_zero);
             }
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             if (mark) mark(user, "rank");
@@ -1694,10 +1741,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         if (splits < 1) splits = 1;
         w.splits = static_cast<int32_t>(splits);
         w.n_items = static_cast<int32_t>(tiles * 2 * splits);
-        int per_sm = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, walk_kern, wg.warps * 32, wg.smem);
-        if (per_sm < 1) per_sm = 1;
-        const int grid = w.n_items < sm_count * per_sm ? w.n_items : sm_count * per_sm;
+        const int grid = w.n_items < sm_count * walk_per_sm ? w.n_items : sm_count * walk_per_sm;
         walk_kern<<<grid, wg.warps * 32, wg.smem, s>>>(w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (mark) mark(user, "walk");
@@ -1734,7 +1778,6 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         if (sliced) {
             a.et = et;
             a.arrive = arrive;
-            if ((e = cudaMemsetAsync(arrive, 0, static_cast<size_t>(n) * 4, s)) != cudaSuccess) return e;
             if ((e = static_cast<cudaError_t>(launch_acc_sliced_cpl(a, sm_count, s))) != cudaSuccess) return e;
         } else if ((e = static_cast<cudaError_t>(launch_acc_cpl(a, sm_count, s))) != cudaSuccess) {
             return e;

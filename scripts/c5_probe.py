@@ -79,3 +79,20 @@ torch.cuda.synchronize()
 pipe = (time.perf_counter() - t0) / 200
 print(f"B={B} device-resident: enqueue p50 {1e6 * np.median(enq):.1f} us | enqueue+sync p50 {1e6 * np.median(syn):.1f} us"
       f" | pipelined {1e6 * pipe:.1f} us/call")
+
+# Python wrapper overhead vs the bare C call (same prebuilt arguments).
+import ctypes as Ct  # noqa: E402
+from paper_2004_08177_b200 import _capi  # noqa: E402
+gs = _capi.Grid(ptrs["rows"], B, F, K, ptrs["cat_t"], ptrs["cat_cols"], None, B, ptrs["sm"], ptrs["mem"], C_,
+                g.sm_col, g.mem_col, 0, ptrs["budgets"])
+op = opts.opts()
+fn = _capi.lib().gd_grid_select_device
+args = (ctx.handle, me.handle, mt.handle, Ct.byref(gs), Ct.byref(op), ptrs["out"], None, None)
+torch.cuda.synchronize()
+bare = []
+for _ in range(200):
+    t0 = time.perf_counter()
+    fn(*args)
+    bare.append(time.perf_counter() - t0)
+    torch.cuda.synchronize()
+print(f"B={B} bare C enqueue p50 {1e6 * np.median(bare):.1f} us")
