@@ -49,6 +49,17 @@
 #include "gd_common.cuh"
 
 namespace gd {
+#ifdef GD_WALK_TRACE
+__device__ unsigned long long g_wtrace[4096][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define WTRACE(k) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_wtrace[blockIdx.x][k] = gtime(); } while (0)
+#else
+#define WTRACE(k) do {} while (0)
+#endif
 namespace {
 
 using namespace dev;
@@ -547,6 +558,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     unsigned char* after_ranks = smem + 128 + NB * buf_bytes + walk_rank_bytes(p.n_cols, TA);
     Job* jobs = reinterpret_cast<Job*>(after_ranks) + warp * kJobCap;
     int4* tables = reinterpret_cast<int4*>(after_ranks + walk_jobs_bytes(blockDim.x >> 5));
+    WTRACE(0);
     const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
     const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
 
@@ -578,6 +590,33 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         for (int j = 0; j + 1 < NB; ++j) produce(j);
     }
     int32_t row_tile = -1, row_model = -1;
+    // The tile's ranks ([col][app], already in that layout in global memory:
+    // a contiguous, coalesced 16-byte copy) by threads [t0, blockDim.x).
+    auto stage_ranks = [&](int32_t tile, int32_t model, int t0) {
+        const int64_t tiles = (p.n_apps + TA - 1) / TA;
+        const int4* src =
+            reinterpret_cast<const int4*>(p.ranks + ((static_cast<int64_t>(model) * tiles + tile) * p.n_cols) * TA);
+        const uint32_t dst = smem_addr(srank);
+        const int n16 = p.n_cols * TA / 8;
+        // cp.async: every 16-byte piece in flight at once (a load -> store
+        // loop would serialise one L2 round trip per iteration).
+        for (int i = static_cast<int>(threadIdx.x) - t0; i >= 0 && i < n16; i += blockDim.x - t0) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * static_cast<uint32_t>(i)),
+                         "l"(src + i)
+                         : "memory");
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        row_tile = tile;
+        row_model = model;
+    };
+    WTRACE(1);
+    if (it_begin < it_end) {
+        // The first item's ranks load while its first stage is planned and in
+        // flight: warp 0 is busy planning, so the other warps copy them.
+        const ItemInfo i0 = item_info(p, it_begin);
+        stage_ranks(i0.tile, i0.model, nwarps > 1 ? 32 : 0);
+        __syncthreads();
+    }
     for (int k = 0;; ++k) {
         const int buf = k % NB;
         if (warp == 0) {
@@ -586,7 +625,9 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
             produce(k + NB - 1);
             __syncwarp();
         }
+        if (k == 0) WTRACE(2);
         mbar_wait(bar0 + 8 * buf, static_cast<uint32_t>(k / NB) & 1u);
+        if (k == 0) WTRACE(3);
         const Stage s = desc[buf];
         if (!s.valid) break;
         const ItemInfo ii = item_info(p, s.item);
@@ -594,17 +635,8 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         const int n_here = static_cast<int>(min(static_cast<int64_t>(TA), p.n_apps - tile0));
         if (ii.tile != row_tile || ii.model != row_model) {
             __syncthreads();  // every warp is done with the previous tile's ranks
-            // Stage the tile's ranks ([col][app], already in that layout in
-            // global memory: a contiguous, coalesced 16-byte copy).
-            const int64_t tiles = (p.n_apps + TA - 1) / TA;
-            const int4* src = reinterpret_cast<const int4*>(
-                p.ranks + ((static_cast<int64_t>(ii.model) * tiles + ii.tile) * p.n_cols) * TA);
-            int4* dst = reinterpret_cast<int4*>(srank);
-            const int n16 = p.n_cols * TA / 8;
-            for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+            stage_ranks(ii.tile, ii.model, 0);
             __syncthreads();
-            row_tile = ii.tile;
-            row_model = ii.model;
         }
 
         const int li = group * 32 + lane;
@@ -645,7 +677,9 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
                 finish_walk<kAllSmem>(p, c0, c, jobs, count, lane, vv[h], w[h], tt[h], src[h].saddr, li, ii.model,
                                       out, tile0);
         }
+        if (k == 0) WTRACE(4);
         if (count > 0) run_jobs<kAllSmem>(p, c0, jobs, count, lane, ii.model, out, tile0);
+        if (k == 0) WTRACE(5);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`
     }
@@ -654,8 +688,11 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
 // Ranks of the batch's rows for both models, laid out as the walk kernel
 // stages them: ranks[m][tile][f][app in tile] (tile = TA apps), value =
 // #{thresholds of model m on feature f that are < x} (NaN: their count); the
-// time model sees the time-encoded categorical columns.  Consecutive threads
-// take consecutive apps of one (m, tile, f), so the stores are coalesced.
+// time model sees the time-encoded categorical columns.  grid_rank_kernel:
+// consecutive threads take consecutive apps of one (m, tile, f), so the stores
+// are coalesced.  Both rank kernels also zero `zero[0, n_zero)` (the batch's
+// walk / accumulate counters).
+//
 // Small batches (latency mode): a warp per rank, 32-ary search -- each round
 // samples the last threshold of 32 equal chunks and keeps the chunk holding
 // the boundary, so ~3 dependent loads replace ~13 of the binary search.
@@ -1737,6 +1774,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;
         const int64_t max_pairs = pe > pt ? pe : pt;
         int64_t splits = (8LL * sm_count + 2 * tiles - 1) / (2 * tiles);
+        splits = env_i64("GDVFS_WALK_SPLITS", splits);
         if (splits > max_pairs) splits = max_pairs;
         if (splits < 1) splits = 1;
         w.splits = static_cast<int32_t>(splits);
@@ -1789,3 +1827,8 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
 }
 
 }  // namespace gd
+#ifdef GD_WALK_TRACE
+extern "C" int gd_debug_walk_trace(unsigned long long* out, int n) {
+    return static_cast<int>(cudaMemcpyFromSymbol(out, gd::g_wtrace, static_cast<size_t>(n) * 64));
+}
+#endif
