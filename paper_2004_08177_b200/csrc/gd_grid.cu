@@ -275,14 +275,13 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
     }
     r.info = kRecFull;
     r.ref = s.groot + (w.n >> 3);
-    // Warp-aggregated allocation among the lanes that got here together.
+    // Warp-aggregated pool allocation among the lanes that got here together,
+    // issued now and consumed at the end: its round trip overlaps the
+    // grandchild walks and the leaf loads.
     const unsigned am = __activemask();
     const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
     uint32_t base = 0;
     if (lane == leader) base = atomicAdd(p.pool_count, static_cast<uint32_t>(__popc(am)));
-    const uint32_t idx = __shfl_sync(am, base, leader) + __popc(am & ((1u << lane) - 1u));
-    if (idx >= p.pool_cap) return r;
-    RTRec* q = p.pool + idx;
     const uint2 left = make_uint2(0u, 0u);
     Walk X[4] = {A, A, B, B};
     if (ac) {
@@ -295,35 +294,48 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
     }
     walk2<kAllSmem>(c, s, ac, X[0], ac, X[1]);
     walk2<kAllSmem>(c, s, bc, X[2], bc, X[3]);
-    q->test[0] = test_mk(w);
-    q->test[1] = ac ? test_mk(A) : left;
-    q->test[2] = bc ? test_mk(B) : left;
+    uint2 test[7];
+    test[0] = test_mk(w);
+    test[1] = ac ? test_mk(A) : left;
+    test[2] = bc ? test_mk(B) : left;
     bool deeper = false;
 #pragma unroll
     for (int k = 0; k < 4; ++k) deeper |= wfeat(X[k].fc) != kFeatLeaf;
+    double leaf[8];
+    int depth = 2;  // 0: deeper than 3 (FULL)
     if (!deeper) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) q->leaf[k] = leaf_value(c, X[k]);
-        q->depth = 2;
-        r.info = kRecTable;
-        r.ref = static_cast<int32_t>(idx);
-        return r;
-    }
+        for (int k = 0; k < 4; ++k) leaf[k] = leaf_value(c, X[k]);
+    } else {
+        depth = 3;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const bool xc = wfeat(X[k].fc) != kFeatLeaf;
-        q->test[3 + k] = xc ? test_mk(X[k]) : left;
-        Walk L = X[k], R = X[k];
-        if (xc) {
-            L = child_walk(X[k], 0);
-            R = child_walk(X[k], 1);
+        for (int k = 0; k < 4; ++k) {
+            const bool xc = wfeat(X[k].fc) != kFeatLeaf;
+            test[3 + k] = xc ? test_mk(X[k]) : left;
+            Walk L = X[k], R = X[k];
+            if (xc) {
+                L = child_walk(X[k], 0);
+                R = child_walk(X[k], 1);
+            }
+            walk2<kAllSmem>(c, s, xc, L, xc, R);
+            if (wfeat(L.fc) != kFeatLeaf || wfeat(R.fc) != kFeatLeaf) depth = 0;
+            if (depth) {
+                leaf[2 * k] = leaf_value(c, L);
+                leaf[2 * k + 1] = leaf_value(c, R);
+            }
         }
-        walk2<kAllSmem>(c, s, xc, L, xc, R);
-        if (wfeat(L.fc) != kFeatLeaf || wfeat(R.fc) != kFeatLeaf) return r;  // deeper than 3: FULL
-        q->leaf[2 * k] = leaf_value(c, L);
-        q->leaf[2 * k + 1] = leaf_value(c, R);
     }
-    q->depth = 3;
+    const uint32_t idx = __shfl_sync(am, base, leader) + __popc(am & ((1u << lane) - 1u));
+    if (depth == 0 || idx >= p.pool_cap) return r;  // FULL (a slot left unused, as a deeper residue)
+    RTRec* q = p.pool + idx;
+    const int nt = depth == 2 ? 3 : 7, nl = depth == 2 ? 4 : 8;
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+        if (k < nt) q->test[k] = test[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < nl) q->leaf[k] = leaf[k];
+    q->depth = depth;
     r.info = kRecTable;
     r.ref = static_cast<int32_t>(idx);
     return r;
@@ -338,29 +350,29 @@ __device__ __forceinline__ void store_rec(TreeRec* dst, const TreeRec& r) {
 // A root walk that stopped at a clock node, queued for resolution so the
 // (divergent) residue walks run with full warps.
 struct Job {
-    int32_t n;       // the clock node (byte offset within the tree)
-    int32_t t;       // tree
-    uint32_t saddr;  // shared address of the tree's window
-    int32_t li;      // app within the tile
+    int32_t n;   // the clock node (byte offset within the tree)
+    int32_t t;   // tree
+    int32_t e;   // the tree's entry in the stage table (roots, window, shared address)
+    int32_t li;  // app within the tile
 };
 constexpr int kJobCap = 64;
 
 // Lanes take queued jobs [0, min(32, count)) and write their records, then
 // the queue's tail moves to the front.
 template <bool kAllSmem>
-__device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, Job* jobs, int& count, int lane,
-                                         int model, TreeRec* out, int64_t tile0) {
+__device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
+                                         int& count, int lane, TreeRec* out, int64_t tile0) {
     const int take = min(32, count);
     if (lane < take) {
         const Job j = jobs[lane];
         WalkCtx c = c0;
         c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * 2);
+        const int4 te = table[j.e];  // shared: no global round trip before the residue walk
         TreeSrc s;
-        s.wroot = __ldg(p.wroots[model] + j.t);
-        s.groot = __ldg(p.roots[model] + j.t);
-        s.win = kAllSmem ? 0xffffffffu
-                         : static_cast<uint32_t>(min(__ldg(p.wroots[model] + j.t + 1) - s.wroot, p.win_nodes));
-        s.saddr = j.saddr;
+        s.wroot = te.x;
+        s.groot = te.y;
+        s.win = kAllSmem ? 0xffffffffu : static_cast<uint32_t>(te.z);
+        s.saddr = static_cast<uint32_t>(te.w);
         Walk w{j.n, 0, 0};
         load_wnode<kAllSmem>(c, s, w);
         store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_residue<kAllSmem>(p, c, s, w));
@@ -378,16 +390,16 @@ __device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0,
 // Queue the walk of one tree if it stopped at a clock node, else store its
 // constant record; run a round of jobs once 32 are pending.
 template <bool kAllSmem>
-__device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const WalkCtx& c, Job* jobs,
-                                            int& count, int lane, bool v, const Walk& w, int32_t t, uint32_t saddr,
+__device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const WalkCtx& c, const int4* table, Job* jobs,
+                                            int& count, int lane, bool v, const Walk& w, int32_t t, int32_t e,
                                             int li, int model, TreeRec* out, int64_t tile0) {
     const bool job = v && wfeat(w.fc) != kFeatLeaf;
     if (v && !job) store_rec(out + rec_index(t, tile0 + li, p.n_apps), TreeRec{kRecConst, w.key, 0, 0u});
     const unsigned m = __ballot_sync(kFull, job);
-    if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, saddr, li};
+    if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, e, li};
     count += __popc(m);
     __syncwarp();
-    if (count >= 32) run_jobs<kAllSmem>(p, c0, jobs, count, lane, model, out, tile0);
+    if (count >= 32) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0);
 }
 
 constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
@@ -418,42 +430,6 @@ __device__ __forceinline__ ItemInfo item_info(const WalkParams& p, int32_t it) {
     return r;
 }
 
-
-// Warp 0 (all lanes, uniform result): the next stage after cursor (it, q),
-// advancing the cursor.  Lane l sizes pair q + l; a stage is the longest
-// prefix of up to 32 pairs whose windows fit one buffer (at least one pair).
-__device__ Stage next_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q, int lane) {
-    while (it < it_end) {
-        const ItemInfo ii = item_info(p, it);
-        if (q < ii.p0) q = ii.p0;
-        if (q >= ii.p1) {
-            ++it;
-            q = -1;
-            continue;
-        }
-        const int32_t nt = p.n_trees[ii.model];
-        const int32_t* wroots = p.wroots[ii.model];
-        const int32_t pr = q + lane;
-        int32_t w = 1 << 20;  // > any stage; 32 of them cannot overflow
-        if (pr < ii.p1) {
-            const int32_t r0 = __ldg(wroots + 2 * pr), r1 = __ldg(wroots + min(2 * pr + 1, nt)),
-                          r2 = __ldg(wroots + min(2 * pr + 2, nt));
-            w = min(r1 - r0, p.win_nodes) + min(r2 - r1, p.win_nodes);
-        }
-        int32_t incl = w;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int32_t o = __shfl_up_sync(kFull, incl, d);
-            if (lane >= d) incl += o;
-        }
-        const bool fits = lane == 0 || (incl <= p.stage_nodes && 2 * (lane + 1) <= kStageTrees);
-        const int n = __popc(__ballot_sync(kFull, fits));
-        const Stage s{it, q, q + n, 1};
-        q += n;
-        return s;
-    }
-    return Stage{0, 0, 0, 0};
-}
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -488,46 +464,77 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 
-// Warp 0: load the windows of stage s into its buffer and arm the buffer's
-// barrier; lane i fills tree 2*q0 + i's table entry {walk root, grid root,
-// window nodes, shared address}.  Whole trees are contiguous, so with
-// kAllSmem the stage is one bulk copy; otherwise each lane copies its window.
+// Warp 0 (all lanes, uniform result): plan the next stage after cursor (it,
+// q), advancing the cursor, and start loading it into buffer `buf_saddr`.
+// Lane l sizes pair q + l; a stage is the longest prefix of up to 32 pairs
+// whose windows fit one buffer (at least one pair).  The same loads give the
+// stage's tree table -- lane l fills the entries {walk root, grid root, window
+// nodes, shared address} of trees 2(q+l) and 2(q+l)+1 -- so planning and
+// issuing cost one round trip.  Whole trees are contiguous, so with kAllSmem
+// the stage is one bulk copy; otherwise each window is copied on its own.
+// Arms the buffer's barrier (or arrives on it for an invalid stage).
 template <bool kAllSmem>
-__device__ void issue_stage(const WalkParams& p, const Stage& s, uint32_t buf_saddr, uint32_t bar, int4* table,
-                            int lane) {
-    const ItemInfo ii = item_info(p, s.item);
-    const int32_t nt = p.n_trees[ii.model];
-    const int32_t* wroots = p.wroots[ii.model];
-    const int32_t* roots = p.roots[ii.model];
-    const WNode* nodes = p.wnodes[ii.model];
-    const int32_t t_end = min(2 * s.q1, nt);
-    uint32_t total = 0;
-    for (int32_t t0 = 2 * s.q0; t0 < t_end; t0 += 32) {
-        const int32_t t = t0 + lane;
-        const bool has = t < t_end;
-        const int32_t wr = has ? __ldg(wroots + t) : 0;
-        const int32_t win = has ? min(__ldg(wroots + t + 1) - wr, p.win_nodes) : 0;
-        int32_t incl = win;
+__device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q, int lane,
+                           uint32_t buf_saddr, uint32_t bar, int4* table, Stage* desc) {
+    while (it < it_end) {
+        const ItemInfo ii = item_info(p, it);
+        if (q < ii.p0) q = ii.p0;
+        if (q >= ii.p1) {
+            ++it;
+            q = -1;
+            continue;
+        }
+        const int32_t nt = p.n_trees[ii.model];
+        const int32_t* wroots = p.wroots[ii.model];
+        const int32_t* roots = p.roots[ii.model];
+        const int32_t pr = q + lane;
+        int32_t w = 1 << 20;  // > any stage; 32 of them cannot overflow
+        int32_t r0 = 0, r1 = 0, r2 = 0, g0 = 0, g1 = 0;
+        if (pr < ii.p1) {
+            r0 = __ldg(wroots + 2 * pr);
+            r1 = __ldg(wroots + min(2 * pr + 1, nt));
+            r2 = __ldg(wroots + min(2 * pr + 2, nt));
+            g0 = __ldg(roots + 2 * pr);
+            g1 = 2 * pr + 1 < nt ? __ldg(roots + 2 * pr + 1) : 0;
+            w = min(r1 - r0, p.win_nodes) + min(r2 - r1, p.win_nodes);
+        }
+        int32_t incl = w;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int32_t o = __shfl_up_sync(kFull, incl, d);
             if (lane >= d) incl += o;
         }
-        const uint32_t off = total + 8u * static_cast<uint32_t>(incl - win);
-        if (has) {
-            table[t - 2 * s.q0] = make_int4(wr, __ldg(roots + t), win, static_cast<int>(buf_saddr + off));
+        const bool fits = lane == 0 || (incl <= p.stage_nodes && 2 * (lane + 1) <= kStageTrees);
+        const int n = __popc(__ballot_sync(kFull, fits));
+        const Stage st{it, q, q + n, 1};
+        q += n;
+        const WNode* nodes = p.wnodes[ii.model];
+        if (lane < n) {
+            const int32_t wa = min(r1 - r0, p.win_nodes), wb = min(r2 - r1, p.win_nodes);
+            const uint32_t off = 8u * static_cast<uint32_t>(incl - w);
+            const int k = 2 * lane;  // table index of tree 2 * pr
+            table[k] = make_int4(r0, g0, wa, static_cast<int>(buf_saddr + off));
+            if (2 * pr + 1 < nt) table[k + 1] = make_int4(r1, g1, wb, static_cast<int>(buf_saddr + off + 8u * wa));
             if (!kAllSmem) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bulk_g2s(buf_saddr + off, nodes + wr, 8u * static_cast<uint32_t>(win), bar);
+                bulk_g2s(buf_saddr + off, nodes + r0, 8u * static_cast<uint32_t>(wa), bar);
+                if (2 * pr + 1 < nt && wb > 0) bulk_g2s(buf_saddr + off + 8u * wa, nodes + r1, 8u * static_cast<uint32_t>(wb), bar);
             }
         }
-        total += 8u * static_cast<uint32_t>(__shfl_sync(kFull, incl, 31));
+        const uint32_t total = 8u * static_cast<uint32_t>(__shfl_sync(kFull, incl, n - 1));
+        const int32_t first = __shfl_sync(kFull, r0, 0);
+        __syncwarp();  // the table entries are visible before lane 0's arrive releases them
+        if (lane == 0) {
+            *desc = st;  // published by the barrier's phase completion
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (kAllSmem) bulk_g2s(buf_saddr, nodes + first, total, bar);
+            mbar_expect_tx(bar, total);
+        }
+        return;
     }
-    __syncwarp();  // the table entries are visible before lane 0's arrive releases them
     if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (kAllSmem) bulk_g2s(buf_saddr, nodes + __ldg(wroots + 2 * s.q0), total, bar);
-        mbar_expect_tx(bar, total);
+        *desc = Stage{0, 0, 0, 0};
+        mbar_arrive(bar);
     }
 }
 
@@ -569,14 +576,8 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     int32_t cur_it = it_begin, cur_q = -1;  // warp 0's schedule cursor
     auto produce = [&](int j) {  // warp 0: plan stage j into buffer j % NB
         const int b = j % NB;
-        const Stage nx = next_stage(p, it_end, cur_it, cur_q, lane);
-        if (lane == 0) desc[b] = nx;
-        if (nx.valid) {
-            issue_stage<kAllSmem>(p, nx, bufs0 + static_cast<uint32_t>(b * buf_bytes), bar0 + 8 * b,
-                                  tables + b * kStageTrees, lane);
-        } else if (lane == 0) {
-            mbar_arrive(bar0 + 8 * b);
-        }
+        plan_stage<kAllSmem>(p, it_end, cur_it, cur_q, lane, bufs0 + static_cast<uint32_t>(b * buf_bytes), bar0 + 8 * b,
+                             tables + b * kStageTrees, desc + b);
     };
     if (threadIdx.x == 0) {
         for (int b = 0; b < NB; ++b) {
@@ -674,11 +675,12 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
             walkn<kAllSmem, NW>(c, src, vv, w);
 #pragma unroll
             for (int h = 0; h < NW; ++h)
-                finish_walk<kAllSmem>(p, c0, c, jobs, count, lane, vv[h], w[h], tt[h], src[h].saddr, li, ii.model,
+                finish_walk<kAllSmem>(p, c0, c, table, jobs, count, lane, vv[h], w[h], tt[h],
+                                      min(tt[h], t_last) - 2 * s.q0, li, ii.model,
                                       out, tile0);
         }
         if (k == 0) WTRACE(4);
-        if (count > 0) run_jobs<kAllSmem>(p, c0, jobs, count, lane, ii.model, out, tile0);
+        if (count > 0) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0);
         if (k == 0) WTRACE(5);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`

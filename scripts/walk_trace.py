@@ -37,3 +37,6 @@ for k, name in enumerate(["start", "init+produce", "ranks", "stage0 ready", "wal
 d = np.diff(rel[:, :6], axis=1)
 for k, name in enumerate(["init+produce", "ranks", "TMA wait", "walks", "jobs"]):
     print(f"  delta {name:12s} median {np.median(d[:, k]):6.2f} p90 {np.percentile(d[:, k], 90):6.2f} max {d[:, k].max():6.2f}")
+slow = np.argsort(-d[:, 3])[:12]
+idx = np.nonzero(used)[0]
+print("slowest walk phases (cta: walks us, jobs us):", [(int(idx[i]), round(float(d[i, 3]), 2), round(float(d[i, 4]), 2)) for i in slow])
