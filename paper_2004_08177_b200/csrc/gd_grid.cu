@@ -929,6 +929,34 @@ __device__ __forceinline__ void add_table(double (&acc)[CPL], const unsigned (&c
     }
 }
 
+// Depth-2 table when every clock of this lane has memory clock mem_l: a test
+// whose mask has no core-clock bits (a memory test, or the always-left
+// filler) has one outcome for the whole lane, so it is resolved once per lane
+// and at most one test remains per clock.  The test kinds are the table's
+// (the same for every lane), so the branches are uniform.
+template <int CPL>
+__device__ __forceinline__ void add_table2_mem_uniform(double (&acc)[CPL], const unsigned (&ck)[CPL], uint32_t sb,
+                                                       unsigned mem_l) {
+    const uint2 t0 = lds_u2(sb);
+    if (t0.x != 0xffffffffu) {  // root resolved per lane: child n, then one test per clock
+        const uint32_t n = 1u + ((mem_l & t0.x) > t0.y ? 1u : 0u);
+        const uint2 tc = lds_u2(sb + n * 8u);
+        const double lv = lds_f64(sb + 64u + (2u * n - 2u) * 8u), rv = lds_f64(sb + 64u + (2u * n - 1u) * 8u);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & tc.x) > tc.y ? rv : lv);
+        return;
+    }
+    const uint2 t1 = lds_u2(sb + 8u), t2 = lds_u2(sb + 16u);
+    if (t1.x != 0xffffffffu && t2.x != 0xffffffffu) {  // both children resolved per lane: one test per clock
+        const double lv = lds_f64(sb + 64u + ((mem_l & t1.x) > t1.y ? 8u : 0u));
+        const double rv = lds_f64(sb + 80u + ((mem_l & t2.x) > t2.y ? 8u : 0u));
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] > t0.y ? rv : lv);
+        return;
+    }
+    add_table<CPL, 2>(acc, ck, sb);
+}
+
 // The group's per-kind tree masks (ballots: warp-uniform, so the per-tree
 // dispatch below is uniform branching).
 struct GroupMasks {
@@ -979,8 +1007,12 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
             }
             __syncwarp();
         }
-        if (lds_u32(sb + 56u) == 2u) add_table<CPL, 2>(acc, ck, sb);
-        else add_table<CPL, 3>(acc, ck, sb);
+        if (lds_u32(sb + 56u) == 2u) {
+            if (mem_uniform) add_table2_mem_uniform<CPL>(acc, ck, sb, mem_l);
+            else add_table<CPL, 2>(acc, ck, sb);
+        } else {
+            add_table<CPL, 3>(acc, ck, sb);
+        }
     } else {
         const int32_t ref = static_cast<int32_t>(lds_u32(ws + RG::kMeta + slotb + 4));
 #pragma unroll
