@@ -7,6 +7,7 @@
 // decisions (job order, clock, predicted E/T bits, status, note) for every
 // SchedulerOptions combination; then models::predict vs gpu::predict and the
 // column-mismatch exception message.  Exit 0 = identical.
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -153,6 +154,25 @@ int main(int argc, char** argv) {
         got_msg = e.what();
     }
     expect(!want_msg.empty() && want_msg == got_msg, "column-mismatch message: '" + got_msg + "'");
+
+    // Wall time of one cold batch (fresh predictors: correlation, row
+    // construction, encoding, prediction, EDF) -- reference vs drop-in.
+    {
+        sched::SchedulerOptions o;
+        o.budget = sched::DeadlineBudget::full_deadline;
+        auto t0 = std::chrono::steady_clock::now();
+        sched::ClockPredictor rp =
+            sched::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog, clusters);
+        auto want = sched::schedule_d_dvfs(workload, rp, exec, o);
+        auto t1 = std::chrono::steady_clock::now();
+        sched::ClockPredictor gp = gpu::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog, clusters);
+        auto got = gpu::schedule_d_dvfs(workload, gp, exec, o);
+        auto t2 = std::chrono::steady_clock::now();
+        for (std::size_t k = 0; k < want.size() && k < got.size(); ++k) expect(same(want[k], got[k]), "timed batch");
+        std::printf("cold batch of %zu jobs: reference %.2f ms, drop-in %.2f ms (incl. model upload)\n",
+                    workload.jobs.size(), std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                    std::chrono::duration<double, std::milli>(t2 - t1).count());
+    }
 
     std::printf("%s: %d option combos x %zu jobs, %d scheduled decisions compared; %d mismatches\n",
                 failures ? "FACADE FAIL" : "FACADE OK", combos, workload.jobs.size(), scheduled, failures);

@@ -2,13 +2,20 @@
 //
 // This is the reference-side binding: it is compiled against the reference's
 // own headers and links into the reference's library, and it reaches the
-// GPU only through the C ABI (gdvfs.h).  Host-side steps that are not part of
-// the data-parallel path (k-means correlation, clustering.cpp:346-411, and the
-// categorical encoding of the few matched records, ingest.cpp:401-439) are the
-// reference's own functions; everything per (app x clock) runs on the device.
+// GPU only through the C ABI (gdvfs.h).  Everything per (app x clock) runs on
+// the device.  The per-job host steps are restructured around
+// what they depend on: correlation (clustering.cpp:346-411) recomputes the
+// catalog's default-clock points, their cluster labels and default times on
+// every call -- here they are computed once per predictor (CatalogIndex) and
+// a query costs one k-means assignment plus a scan of the catalog apps; and a
+// job's candidate rows (scheduler.cpp:330-359) depend only on the catalog app
+// it correlates to, so the nearest-record substitution, the categorical
+// encoding (the reference's apply_encoding, ingest.cpp:401-439) and the GPU
+// evaluation run once per distinct matched app, not once per job.
 #include "gpudvfs_b200/gpu_api.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <memory>
@@ -122,6 +129,83 @@ int column_of(const std::vector<std::string>& cols, const std::string& name) {
     return it == cols.end() ? -1 : static_cast<int>(it - cols.begin());
 }
 
+// The catalog side of cluster::correlate (clustering.cpp:346-411), computed
+// once: default-clock points, each catalog app's cluster label and
+// default-clock time, and each app's records in catalog order.
+struct CatalogIndex {
+    struct Candidate {
+        std::string app_id;
+        double time_s = 0.0;
+        int label = -1;
+    };
+    bool ok = false;  // false: correlate would throw for every query
+    cluster::PointMatrix points;
+    std::vector<Candidate> candidates;
+    std::map<std::string, std::vector<std::size_t>> records_of;
+
+    void build(const Dataset& catalog, const cluster::KMeansModel& clusters) {
+        for (std::size_t i = 0; i < catalog.records.size(); ++i) records_of[catalog.records[i].app_id].push_back(i);
+        if (catalog.records.empty()) return;
+        try {
+            points = cluster::default_clock_points(catalog);
+            for (std::size_t i = 0; i < points.rows.size(); ++i) {
+                Candidate c;
+                c.app_id = points.ids[i];
+                c.label = clusters.assign(points.rows[i], points.columns);
+                for (std::size_t r : records_of[c.app_id]) {  // first default-clock record, catalog order
+                    if (catalog.records[r].clock == catalog.device.default_clock) {
+                        c.time_s = catalog.records[r].time_s;
+                        break;
+                    }
+                }
+                candidates.push_back(std::move(c));
+            }
+            ok = true;
+        } catch (const std::exception&) {
+            ok = false;
+        }
+    }
+
+    // correlate(...).matched_app for `query`; throws where correlate throws.
+    const std::string& matched_app(const cluster::KMeansModel& clusters, const Dataset& catalog,
+                                   const ProfileRecord& query) const {
+        if (catalog.records.empty()) throw std::invalid_argument("correlate: catalog is empty");
+        if (query.clock != catalog.device.default_clock) {
+            throw std::invalid_argument("correlate: query record must be at the device default clock");
+        }
+        if (!ok) throw std::invalid_argument("correlate: catalog points unavailable");
+        std::vector<double> row;
+        row.reserve(points.columns.size());
+        for (const auto& name : points.columns) {
+            auto it = query.features.numeric.find(name);
+            if (it == query.features.numeric.end()) {
+                throw std::invalid_argument("correlate: query lacks numeric feature '" + name + "'");
+            }
+            row.push_back(it->second);
+        }
+        const int label = clusters.assign(row, points.columns);
+        auto better = [&](const Candidate& a, const Candidate& b) {  // clustering.cpp:384-389
+            const double da = std::abs(query.time_s - a.time_s), db = std::abs(query.time_s - b.time_s);
+            if (da != db) return da < db;
+            return a.app_id < b.app_id;
+        };
+        const Candidate* best = nullptr;
+        for (const auto& c : candidates) {
+            if (c.label != label || c.app_id == query.app_id) continue;
+            if (best == nullptr || better(c, *best)) best = &c;
+        }
+        if (best == nullptr) {  // singleton cluster fallback (clustering.cpp:396-403)
+            for (const auto& c : candidates) {
+                if (best == nullptr || better(c, *best)) best = &c;
+            }
+        }
+        if (best == nullptr) throw std::invalid_argument("correlate: no candidates");
+        return best->app_id;
+    }
+};
+
+using ClockTable = std::map<ClockSet, sched::ClockPrediction>;
+
 // ---------------------------------------------------------------------------
 // The GPU-backed ClockPredictor (replaces ModelPredictorState,
 // scheduler.cpp:304-371).
@@ -131,57 +215,74 @@ struct GpuPredictorState {
     ingest::EncodingMetadata energy_encoding, time_encoding;
     Dataset catalog;
     cluster::KMeansModel clusters;
+    CatalogIndex index;
     std::unique_ptr<ModelHandle> ge, gt;
     std::vector<ClockSet> clocks;
     std::vector<int32_t> sm, mem;
-    std::map<std::string, std::map<ClockSet, sched::ClockPrediction>> cache;
-    std::set<std::string> failed;
+    std::map<std::string, std::shared_ptr<const ClockTable>> cache;  // per job app
+    std::set<std::string> failed;                                     // per job app
+    std::map<std::string, std::shared_ptr<const ClockTable>> by_match;  // per matched catalog app
+    std::set<std::string> match_failed;
     bool columns_ok = true;
 
-    // One batched launch for every not-yet-seen app among `jobs`.
+    // One batched launch for every not-yet-seen matched app among `jobs`.
     void prime(const std::vector<const Job*>& jobs) {
         struct Pending {
-            std::string app_id;
+            std::string app_id;  // the matched catalog app
             std::vector<ProfileRecord> records;
             std::vector<int32_t> rec_local;  // per catalog clock
         };
+        std::vector<std::pair<std::string, std::string>> resolved;  // (job app, matched app)
         std::vector<Pending> todo;
         std::set<std::string> queued;
         for (const Job* job : jobs) {
-            if (cache.count(job->app_id) || failed.count(job->app_id) || queued.count(job->app_id)) continue;
-            queued.insert(job->app_id);
+            if (cache.count(job->app_id) || failed.count(job->app_id)) continue;
+            std::string m;
             try {
-                // scheduler.cpp:330-359: correlated app, its records, nearest
-                // profiled record per catalog clock.
-                cluster::CorrelationResult match = cluster::correlate(clusters, catalog, job->default_profile);
-                Pending p;
-                p.app_id = job->app_id;
-                for (const auto& r : catalog.records) {
-                    if (r.app_id == match.matched_app) p.records.push_back(r);
-                }
-                if (p.records.empty()) throw data_error("correlated app has no records");
-                for (const ClockSet& clock : clocks) {
-                    std::size_t nearest = 0;
-                    auto dist = [&](std::size_t i) {
-                        return std::make_pair(std::abs(p.records[i].clock.mem_clock_mhz - clock.mem_clock_mhz),
-                                              std::abs(p.records[i].clock.sm_clock_mhz - clock.sm_clock_mhz));
-                    };
-                    for (std::size_t i = 0; i < p.records.size(); ++i) {
-                        if (dist(i) < dist(nearest)) nearest = i;
-                    }
-                    p.rec_local.push_back(static_cast<int32_t>(nearest));
-                }
-                todo.push_back(std::move(p));
+                m = index.matched_app(clusters, catalog, job->default_profile);
             } catch (const std::exception&) {
                 failed.insert(job->app_id);
+                continue;
             }
+            resolved.emplace_back(job->app_id, m);
+            if (by_match.count(m) || match_failed.count(m) || queued.count(m)) continue;
+            queued.insert(m);
+            // scheduler.cpp:330-359: the matched app's records and the nearest
+            // profiled record per catalog clock.
+            Pending p;
+            p.app_id = m;
+            for (std::size_t r : index.records_of[m]) p.records.push_back(catalog.records[r]);
+            if (p.records.empty()) {
+                match_failed.insert(m);
+                continue;
+            }
+            for (const ClockSet& clock : clocks) {
+                std::size_t nearest = 0;
+                auto dist = [&](std::size_t i) {
+                    return std::make_pair(std::abs(p.records[i].clock.mem_clock_mhz - clock.mem_clock_mhz),
+                                          std::abs(p.records[i].clock.sm_clock_mhz - clock.sm_clock_mhz));
+                };
+                for (std::size_t i = 0; i < p.records.size(); ++i) {
+                    if (dist(i) < dist(nearest)) nearest = i;
+                }
+                p.rec_local.push_back(static_cast<int32_t>(nearest));
+            }
+            todo.push_back(std::move(p));
         }
         if (!columns_ok) {
-            for (const auto& p : todo) failed.insert(p.app_id);
-            return;
+            for (const auto& p : todo) match_failed.insert(p.app_id);
+            todo.clear();
         }
-        if (todo.empty()) return;
+        if (!todo.empty()) evaluate(todo);
+        for (const auto& [job_app, m] : resolved) {
+            auto it = by_match.find(m);
+            if (it == by_match.end()) failed.insert(job_app);
+            else cache[job_app] = it->second;
+        }
+    }
 
+    template <class P>
+    void evaluate(std::vector<P>& todo) {
         const auto& cols = energy_encoding.columns;
         const int F = static_cast<int>(cols.size());
         std::vector<int32_t> cat_cols;
@@ -189,7 +290,7 @@ struct GpuPredictorState {
         const int K = static_cast<int>(cat_cols.size());
         std::vector<double> rows, cat_t, budgets;
         std::vector<int32_t> rec_of_clock;
-        std::vector<Pending*> batch;
+        std::vector<P*> batch;
         for (auto& p : todo) {
             try {
                 ingest::EncodedMatrix xe = ingest::apply_encoding(energy_encoding, p.records);
@@ -203,7 +304,7 @@ struct GpuPredictorState {
                 budgets.push_back(0.0);
                 batch.push_back(&p);
             } catch (const std::exception&) {
-                failed.insert(p.app_id);
+                match_failed.insert(p.app_id);
             }
         }
         if (batch.empty()) return;
@@ -229,11 +330,12 @@ struct GpuPredictorState {
         gd_select_opts o{GD_MODE_TEXT, GD_OBJECTIVE_ENERGY, 0, 0};
         check(gd_grid_select(context(), ge->m, gt->m, &g, &o, dec.data(), e.data(), t.data()));
         for (int64_t a = 0; a < A; ++a) {
-            auto& per_clock = cache[batch[static_cast<std::size_t>(a)]->app_id];
+            auto table = std::make_shared<ClockTable>();
             for (int32_t c = 0; c < C; ++c) {
-                per_clock[clocks[static_cast<std::size_t>(c)]] =
+                (*table)[clocks[static_cast<std::size_t>(c)]] =
                     sched::ClockPrediction{e[static_cast<std::size_t>(a * C + c)], t[static_cast<std::size_t>(a * C + c)]};
             }
+            by_match[batch[static_cast<std::size_t>(a)]->app_id] = std::move(table);
         }
     }
 };
@@ -248,8 +350,8 @@ struct GpuPredictorFn {
             hit = state->cache.find(job.app_id);
             if (hit == state->cache.end()) return std::nullopt;
         }
-        auto it = hit->second.find(clock);
-        if (it == hit->second.end()) return std::nullopt;
+        auto it = hit->second->find(clock);
+        if (it == hit->second->end()) return std::nullopt;
         return it->second;
     }
 };
@@ -304,6 +406,7 @@ sched::ClockPredictor make_model_predictor(models::FittedModel energy_model, ing
     } catch (const std::invalid_argument&) {
         s->columns_ok = false;
     }
+    s->index.build(s->catalog, s->clusters);
     s->ge = upload(s->energy_model);
     s->gt = upload(s->time_model);
     s->clocks = clock_catalog(s->catalog.device);
