@@ -45,9 +45,11 @@ namespace {
 
 constexpr size_t kStageLimit = 256 << 10;  // host-buffer calls whose inputs fit are staged
 
-// One stream-ordered scratch allocation carved into aligned pieces.
+// One stream-ordered scratch allocation carved into aligned pieces; with a
+// gd_pbuf it is that persistent buffer (grown when too small) instead.
 struct Scratch {
     cudaStream_t stream;
+    gd_pbuf* keep = nullptr;
     char* base = nullptr;
     size_t size = 0;
     std::vector<std::pair<size_t, size_t>> pieces;  // offset, bytes
@@ -59,9 +61,34 @@ struct Scratch {
         return pieces.size() - 1;
     }
     void* ptr(size_t i) const { return pieces[i].second ? base + pieces[i].first : nullptr; }
-    cudaError_t alloc() { return size ? cudaMallocAsync(reinterpret_cast<void**>(&base), size, stream) : cudaSuccess; }
+    cudaError_t alloc() {
+        if (!size) return cudaSuccess;
+        if (!keep) return cudaMallocAsync(reinterpret_cast<void**>(&base), size, stream);
+        cudaError_t e = cudaSuccess;
+        if (!keep->ev && (e = cudaEventCreateWithFlags(&keep->ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+        if (keep->stream && keep->stream != stream && (e = cudaStreamWaitEvent(stream, keep->ev, 0)) != cudaSuccess) {
+            return e;
+        }
+        if (size > keep->cap) {
+            if (keep->base) cudaFreeAsync(keep->base, stream);
+            keep->base = nullptr;
+            keep->cap = 0;
+            const size_t cap = size + size / 4;
+            if ((e = cudaMallocAsync(reinterpret_cast<void**>(&keep->base), cap, stream)) != cudaSuccess) return e;
+            keep->cap = cap;
+        }
+        base = keep->base;
+        return cudaSuccess;
+    }
     ~Scratch() {
-        if (base) cudaFreeAsync(base, stream);
+        if (keep) {
+            if (base) {
+                cudaEventRecord(keep->ev, stream);
+                keep->stream = stream;
+            }
+        } else if (base) {
+            cudaFreeAsync(base, stream);
+        }
     }
 };
 
@@ -330,7 +357,7 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.objective = o.objective;
     p.best_effort = o.best_effort;
     if (g.n_apps == 0) return GD_OK;
-    Scratch s{ctx->stream};
+    Scratch s{ctx->stream, &ctx->pbuf[0]};
     const size_t bytes = gd::grid_scratch_bytes(p, general);
     const size_t i_scr = s.add(bytes);
     GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
@@ -398,6 +425,10 @@ int gd_ctx_destroy(gd_ctx* ctx) {
         cudaEventDestroy(ctx->stage_ev);
     }
     if (ctx->stage) cudaFreeHost(ctx->stage);
+    for (gd_pbuf& b : ctx->pbuf) {
+        if (b.ev) cudaEventDestroy(b.ev);
+        if (b.base) cudaFree(b.base);
+    }
     delete ctx;
     return GD_OK;
 }
@@ -658,7 +689,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
             }
         }
     }
-    Scratch s{ctx->stream};
+    Scratch s{ctx->stream, &ctx->pbuf[1]};
     const size_t i_rows = s.add(static_cast<size_t>(R) * g->n_cols * sizeof(double));
     const size_t i_cat = s.add(static_cast<size_t>(R) * g->n_cat * sizeof(double));
     const size_t i_catc = s.add(static_cast<size_t>(g->n_cat) * sizeof(int32_t));

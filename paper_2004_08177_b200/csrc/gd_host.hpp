@@ -10,6 +10,16 @@
 #include "gd_device.cuh"
 #include "gdvfs.h"
 
+// A device buffer kept across calls (grow-only): the latency path pays no
+// cudaMallocAsync / cudaFreeAsync per call.  `ev` marks the last use, so a
+// call on a different stream first waits for it.
+struct gd_pbuf {
+    char* base = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
 struct gd_ctx {
     int device = 0;
     int sm_count = 148;
@@ -25,6 +35,7 @@ struct gd_ctx {
     char* stage = nullptr;
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev = nullptr;
+    gd_pbuf pbuf[2];  // 0: grid kernel scratch, 1: host-buffer call inputs / outputs
 };
 
 struct gd_model {
