@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -45,6 +46,11 @@ namespace {
 
 constexpr size_t kStageLimit = 256 << 10;  // host-buffer calls whose inputs fit are staged
 
+uint64_t next_model_uid() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+}
+
 // One stream-ordered scratch allocation carved into aligned pieces; with a
 // gd_pbuf it is that persistent buffer (grown when too small) instead.
 struct Scratch {
@@ -76,13 +82,16 @@ struct Scratch {
             const size_t cap = size + size / 4;
             if ((e = cudaMallocAsync(reinterpret_cast<void**>(&keep->base), cap, stream)) != cudaSuccess) return e;
             keep->cap = cap;
+            ++keep->generation;
         }
         base = keep->base;
         return cudaSuccess;
     }
     ~Scratch() {
         if (keep) {
-            if (base) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(stream, &cs);
+            if (base && cs == cudaStreamCaptureStatusNone) {  // (a captured replay reuses the same stream)
                 cudaEventRecord(keep->ev, stream);
                 keep->stream = stream;
             }
@@ -425,6 +434,8 @@ int gd_ctx_destroy(gd_ctx* ctx) {
         cudaEventDestroy(ctx->stage_ev);
     }
     if (ctx->stage) cudaFreeHost(ctx->stage);
+    for (gd_graph_entry& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+    if (ctx->out_stage) cudaFreeHost(ctx->out_stage);
     for (gd_pbuf& b : ctx->pbuf) {
         if (b.ev) cudaEventDestroy(b.ev);
         if (b.base) cudaFree(b.base);
@@ -484,6 +495,7 @@ int gd_model_upload_gbt(gd_ctx* ctx, const gd_forest_view* f, double base, doubl
         return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_upload_gbt: bad tree offsets");
     }
     auto* m = new gd_model;
+    m->uid = next_model_uid();
     m->ctx = ctx;
     m->kind = GD_KIND_GBT;
     m->target = target;
@@ -522,6 +534,7 @@ int gd_model_upload_linear(gd_ctx* ctx, const double* coef, int32_t n_cols, doub
     if (rc) return rc;
     if (kind != GD_KIND_OLS && kind != GD_KIND_LASSO) return set_error(GD_ERR_INVALID_ARGUMENT, "bad linear kind");
     auto* m = new gd_model;
+    m->uid = next_model_uid();
     m->ctx = ctx;
     m->kind = kind;
     m->target = target;
@@ -545,6 +558,7 @@ int gd_model_load_file(gd_ctx* ctx, const char* path, gd_model** out) {
     int rc = activate_opt(ctx);
     if (rc) return rc;
     auto* m = new gd_model;
+    m->uid = next_model_uid();
     m->ctx = ctx;
     rc = gdh::parse_model_file(path, *m);
     if (!rc) rc = upload_model(m);
@@ -657,6 +671,82 @@ int gd_grid_select_device(gd_ctx* ctx, const gd_model* me, const gd_model* mt, c
     return grid_impl(ctx, me, mt, *g, *o, d_out, d_e, d_t, rows_t);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Small host-buffer calls (the configs[4] stream) replay a captured graph:
+// one cudaGraphLaunch instead of a staged copy, three kernel launches and a
+// result copy issued one by one (GDVFS_GRAPHS=0 disables).
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("GDVFS_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+bool same_key(const gd_graph_entry& a, const gd_graph_entry& b) {
+    return a.me == b.me && a.mt == b.mt && a.n_apps == b.n_apps && a.n_clocks == b.n_clocks && a.n_cols == b.n_cols &&
+           a.n_cat == b.n_cat && a.sm_col == b.sm_col && a.mem_col == b.mem_col && a.mode == b.mode &&
+           a.objective == b.objective && a.best_effort == b.best_effort && a.stream == b.stream;
+}
+
+gd_graph_entry* find_graph(gd_ctx* ctx, const gd_graph_entry& key) {
+    for (size_t i = 0; i < ctx->graphs.size(); ++i) {
+        gd_graph_entry& e = ctx->graphs[i];
+        if (!same_key(e, key)) continue;
+        if (e.gen0 != ctx->pbuf[0].generation || e.gen1 != ctx->pbuf[1].generation) {  // buffers moved
+            cudaGraphExecDestroy(e.exec);
+            ctx->graphs.erase(ctx->graphs.begin() + static_cast<std::ptrdiff_t>(i));
+            return nullptr;
+        }
+        return &e;
+    }
+    return nullptr;
+}
+
+// Capture the pipeline of a call that just ran (so every buffer is sized and
+// every model structure built): staged inputs -> kernels -> decisions into
+// ctx->out_stage.  Failures leave no entry (the normal path keeps working).
+void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& dg, const gd_select_opts& o,
+                   gd_graph_entry key, void* dev_in, size_t in_end, gd_decision* dev_out) {
+    const size_t out_bytes = static_cast<size_t>(dg.n_apps) * sizeof(gd_decision);
+    if (!ctx->out_stage && cudaHostAlloc(reinterpret_cast<void**>(&ctx->out_stage), kStageLimit, cudaHostAllocDefault) !=
+                               cudaSuccess) {
+        ctx->out_stage = nullptr;
+        cudaGetLastError();
+        return;
+    }
+    const int64_t launches = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+        ok = cudaMemcpyAsync(dev_in, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
+        ok = ok && grid_impl(ctx, me, mt, dg, o, dev_out, nullptr, nullptr, nullptr, false) == GD_OK;
+        ok = ok && cudaMemcpyAsync(ctx->out_stage, dev_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
+        ok = (cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess) && ok;
+    }
+    ctx->launches = launches;
+    cudaGraphExec_t exec = nullptr;
+    if (ok && graph) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (!ok || !exec) return;
+    key.gen0 = ctx->pbuf[0].generation;
+    key.gen1 = ctx->pbuf[1].generation;
+    key.exec = exec;
+    if (ctx->graphs.size() >= 8) {
+        cudaGraphExecDestroy(ctx->graphs.front().exec);
+        ctx->graphs.erase(ctx->graphs.begin());
+    }
+    ctx->graphs.push_back(key);
+}
+
+}  // namespace
+
+extern "C" {
+
 int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
                    gd_decision* out, double* e_out, double* t_out) {
     int rc = activate(ctx);
@@ -701,17 +791,47 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     const size_t i_e = s.add(e_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
     const size_t i_t = s.add(t_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
     const size_t i_rt = s.add(g->rec_of_clock ? static_cast<size_t>(R) * g->n_cols * sizeof(double) : 0);
+    const size_t in_end0 = s.pieces[i_bud].first + s.pieces[i_bud].second;
+    const bool graphable = graphs_enabled() && !ctx->timing && !g->rec_of_clock && !e_out && !t_out &&
+                           in_end0 <= kStageLimit && static_cast<size_t>(A) * sizeof(gd_decision) <= kStageLimit;
+    gd_graph_entry key;
+    key.me = me->uid;
+    key.mt = mt->uid;
+    key.n_apps = A;
+    key.n_clocks = static_cast<int32_t>(C);
+    key.n_cols = g->n_cols;
+    key.n_cat = g->n_cat;
+    key.sm_col = g->sm_col;
+    key.mem_col = g->mem_col;
+    key.mode = o->mode;
+    key.objective = o->objective;
+    key.best_effort = o->best_effort;
+    key.stream = ctx->stream;
+    const std::pair<size_t, const void*> inputs[] = {{i_rows, g->rows},        {i_cat, g->cat_t},
+                                                     {i_catc, g->cat_cols},    {i_rec, g->rec_of_clock},
+                                                     {i_sm, g->sm_clock},      {i_mem, g->mem_clock},
+                                                     {i_bud, g->budgets}};
+    if (graphable && ctx->stage) {
+        if (gd_graph_entry* hit = find_graph(ctx, key)) {
+            GD_CUDA(cudaEventSynchronize(ctx->stage_ev), "stage reuse");
+            for (const auto& in : inputs) {
+                if (s.pieces[in.first].second) std::memcpy(ctx->stage + s.pieces[in.first].first, in.second, s.pieces[in.first].second);
+            }
+            GD_CUDA(cudaGraphLaunch(hit->exec, ctx->stream), "cudaGraphLaunch");
+            ctx->launches += 3;
+            GD_CUDA(cudaEventRecord(ctx->stage_ev, ctx->stream), "stage event record");
+            GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
+            std::memcpy(out, ctx->out_stage, static_cast<size_t>(A) * sizeof(gd_decision));
+            return GD_OK;
+        }
+    }
     GD_CUDA(s.alloc(), "cudaMallocAsync");
     if (ctx->timing) timing_begin(ctx);
     // Inputs occupy the scratch prefix [0, in_end).  Small calls (the online
     // stream's 64-job batches) pack them into pinned staging with the same
     // offsets and move them in ONE copy: per-copy latency, not bandwidth,
     // bounds them.  Large calls copy each array straight from the caller.
-    const size_t in_end = s.pieces[i_bud].first + s.pieces[i_bud].second;
-    const std::pair<size_t, const void*> inputs[] = {{i_rows, g->rows},        {i_cat, g->cat_t},
-                                                     {i_catc, g->cat_cols},    {i_rec, g->rec_of_clock},
-                                                     {i_sm, g->sm_clock},      {i_mem, g->mem_clock},
-                                                     {i_bud, g->budgets}};
+    const size_t in_end = in_end0;
     if (in_end <= kStageLimit) {
         if (!ctx->stage_ev) GD_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming), "stage event");
         GD_CUDA(cudaEventSynchronize(ctx->stage_ev), "stage reuse");
@@ -768,6 +888,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     }
     if (ctx->timing) timing_mark(ctx, "d2h");
     GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
+    if (graphable && ctx->stage) capture_graph(ctx, me, mt, dg, *o, key, s.base, in_end, static_cast<gd_decision*>(s.ptr(i_out)));
     return GD_OK;
 }
 

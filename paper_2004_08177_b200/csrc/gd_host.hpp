@@ -16,8 +16,21 @@
 struct gd_pbuf {
     char* base = nullptr;
     size_t cap = 0;
+    uint64_t generation = 0;  // bumped when the buffer moves (captured graphs hold its address)
     cudaEvent_t ev = nullptr;
     cudaStream_t stream = nullptr;
+};
+
+// A captured small-call pipeline (staged H2D -> rank -> walk -> accumulate
+// -> D2H into pinned staging), replayed with one cudaGraphLaunch.
+struct gd_graph_entry {
+    uint64_t me = 0, mt = 0;  // model uids
+    int64_t n_apps = 0;
+    int32_t n_clocks = 0, n_cols = 0, n_cat = 0, sm_col = 0, mem_col = 0;
+    int32_t mode = 0, objective = 0, best_effort = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t gen0 = 0, gen1 = 0;  // pbuf generations at capture
+    cudaGraphExec_t exec = nullptr;
 };
 
 struct gd_ctx {
@@ -36,10 +49,13 @@ struct gd_ctx {
     size_t stage_bytes = 0;
     cudaEvent_t stage_ev = nullptr;
     gd_pbuf pbuf[2];  // 0: grid kernel scratch, 1: host-buffer call inputs / outputs
+    char* out_stage = nullptr;  // pinned, kStageLimit bytes: decisions of graph replays
+    std::vector<gd_graph_entry> graphs;  // most recent last
 };
 
 struct gd_model {
     gd_ctx* ctx = nullptr;
+    uint64_t uid = 0;  // process-unique (graph cache keys survive address reuse)
     int32_t kind = GD_KIND_GBT;
     int32_t target = GD_TARGET_ENERGY;
     int32_t n_cols = 0;

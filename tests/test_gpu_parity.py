@@ -132,6 +132,34 @@ def test_k2_grid_predictions_and_decisions_vs_oracle(ctx, name, sliced, monkeypa
         assert decisions_equal(got, want), (name, combo)
 
 
+def test_k2_graph_replay_stream_vs_oracle(ctx):
+    """Decisions-only small calls are captured once per shape and replayed as
+    a CUDA graph (the configs[4] stream): successive windows, both selection
+    modes, a buffer-growing large call in between (the captured addresses
+    move: the graph must be rebuilt), and a second model pair."""
+    sc = W.make_scenario("replay", 1200, "gtx980", 60, 8, seed=31, w_clk=0.08)
+    g = sc.grid
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, g, np.ones(g.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=3)
+
+    def window(lo, n):
+        return W.GridInputs(np.ascontiguousarray(g.rows[lo:lo + n]), np.ascontiguousarray(g.cat_t[lo:lo + n]),
+                            g.cat_cols.astype(np.int32), g.sm.astype(np.int32), g.mem.astype(np.int32), g.sm_col,
+                            g.mem_col), np.ascontiguousarray(budgets[lo:lo + n])
+
+    other = W.make_scenario("replay2", 8, "gtx980", 45, 7, seed=77, w_clk=0.1)
+    for pair in range(2):
+        f_e, f_t = (sc.energy, sc.time) if pair == 0 else (other.energy, other.time)
+        me, mt = gd.Model.from_forest(f_e, ctx), gd.Model.from_forest(f_t, ctx)
+        for combo in [(0, 1, 0, 0), (1, 1, 1, 1)]:
+            mode, _, obj, be = combo
+            for k, n in enumerate([64, 64, 64, 1000, 64, 64]):
+                gw, bw = window((k * 64) % 200, n)
+                got = gd.grid_select(me, mt, gw, bw, opts_of(*combo))
+                want, _, _ = O.oracle_grid(f_e, f_t, gw, bw, mode, obj, be)
+                assert decisions_equal(got, want), (pair, combo, k)
+
+
 # Internal paths of the walk / accumulate pipeline forced through knobs (the
 # library reads them per call): several batches, small shared-memory windows
 # (walks continue from global memory), residue-table pool overflow (FULL
