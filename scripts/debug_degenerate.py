@@ -1,3 +1,4 @@
+"""Debug helper: the degenerate-model grid cases of test_k2_degenerate_models_and_values, one at a time, with the first mismatching (app, clock)."""
 import sys; sys.path.insert(0,'.'); sys.path.insert(0,'tests')
 import numpy as np, dataclasses
 import paper_2004_08177_b200 as gd
