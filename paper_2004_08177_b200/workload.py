@@ -264,10 +264,15 @@ class Scenario:
     seed: int
 
 
-def make_scenario(name: str, n_apps: int, catalog: str, n_trees: int, depth: int, seed: int = 1234,
+def make_scenario(name: str, n_apps: int, catalog, n_trees: int, depth: int, seed: int = 1234,
                   w_clk: float = 0.04, leaf_prob: float = 0.0) -> Scenario:
-    """A complete synthetic (apps, catalog, E/T ensembles) configuration."""
-    sm, mem = CATALOGS[catalog]()
+    """A complete synthetic (apps, catalog, E/T ensembles) configuration.
+    `catalog`: a CATALOGS name or an explicit (sm, mem) pair of int32 arrays
+    in the order the candidates are to be evaluated (any order)."""
+    if isinstance(catalog, str):
+        sm, mem = CATALOGS[catalog]()
+    else:
+        sm, mem = (np.ascontiguousarray(x, dtype=np.int32) for x in catalog)
     rng = np.random.default_rng(seed)
     cols = _ColumnModel(rng, N_COLS, CAT_COLS, sm, mem, SM_COL, MEM_COL)
     fe = make_forest(cols, n_trees, depth, 0, seed + 1, w_clk, leaf_prob)

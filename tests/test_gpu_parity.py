@@ -160,6 +160,40 @@ def test_k2_graph_replay_stream_vs_oracle(ctx):
                 assert decisions_equal(got, want), (pair, combo, k)
 
 
+@pytest.mark.parametrize("seed", range(64))
+def test_k2_fuzz_catalogs_and_shapes_vs_oracle(ctx, seed):
+    """Random catalogs (any size up to 512, 1..40 memory clocks, arbitrary
+    order or the reference's (mem, sm) order, duplicate pairs allowed),
+    random tree shapes / clock-split rates, batch sizes on both sides of the
+    latency-mode switch, random selection options: predictions and decisions
+    bit-identical to the oracle, with and without the E/T tables (the
+    decisions-only calls also exercise the graph replay)."""
+    rng = np.random.default_rng(1000 + seed)
+    C = int(rng.choice([1, 2, 5, 31, 32, 33, 64, 100, 267, 300, 512]))
+    n_mem = int(rng.integers(1, min(C, 40) + 1))
+    mems = rng.choice(np.arange(300, 9000, 7), size=n_mem, replace=False)
+    sm = rng.integers(100, 2500, size=C).astype(np.int32)
+    mem = rng.choice(mems, size=C).astype(np.int32)
+    if rng.random() < 0.5:
+        order = np.lexsort((sm, mem))
+        sm, mem = sm[order], mem[order]
+    n_apps = int(rng.choice([1, 7, 64, 255, 257, 600]))
+    sc = W.make_scenario("fuzz", n_apps, (sm, mem), int(rng.integers(1, 80)), int(rng.integers(1, 11)), seed=seed,
+                         w_clk=float(rng.choice([0.0, 0.05, 0.2, 0.5])), leaf_prob=float(rng.choice([0.0, 0.3])))
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(n_apps))
+    budgets = W.deadlines_from_times(t0, seed=seed)
+    for _ in range(2):
+        combo = tuple(int(x) for x in rng.integers(0, 2, size=4))
+        mode, _, obj, be = combo
+        want, we, wt = O.oracle_grid(sc.energy, sc.time, sc.grid, budgets, mode, obj, be)
+        got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, opts_of(*combo), return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt)), (seed, combo)
+        assert decisions_equal(got, want), (seed, combo)
+        for _ in range(2):
+            assert decisions_equal(gd.grid_select(me, mt, sc.grid, budgets, opts_of(*combo)), want), (seed, combo)
+
+
 # Internal paths of the walk / accumulate pipeline forced through knobs (the
 # library reads them per call): several batches, small shared-memory windows
 # (walks continue from global memory), residue-table pool overflow (FULL
