@@ -846,11 +846,37 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
         GD_CUDA(cudaMemcpyAsync(s.base, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream), "H2D staged inputs");
         GD_CUDA(cudaEventRecord(ctx->stage_ev, ctx->stream), "stage event record");
     } else {
-        for (const auto& in : inputs) {
-            if (!s.pieces[in.first].second) continue;
-            GD_CUDA(cudaMemcpyAsync(s.ptr(in.first), in.second, s.pieces[in.first].second, cudaMemcpyHostToDevice,
+        // The rows go straight from the caller's buffer; the rest (scratch
+        // range [cat_t, budgets]) is packed into the pinned staging while
+        // that copy runs and follows in one more copy, when it fits.
+        const size_t rest0 = s.pieces[i_cat].first, rest = in_end - rest0;
+        if (s.pieces[i_rows].second) {
+            GD_CUDA(cudaMemcpyAsync(s.ptr(i_rows), g->rows, s.pieces[i_rows].second, cudaMemcpyHostToDevice,
                                     ctx->stream),
-                    "H2D grid input");
+                    "H2D rows");
+        }
+        if (rest <= kStageLimit) {
+            if (!ctx->stage_ev) GD_CUDA(cudaEventCreateWithFlags(&ctx->stage_ev, cudaEventDisableTiming), "stage event");
+            GD_CUDA(cudaEventSynchronize(ctx->stage_ev), "stage reuse");
+            if (!ctx->stage) {
+                GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage), kStageLimit, cudaHostAllocDefault),
+                        "cudaHostAlloc(stage)");
+                ctx->stage_bytes = kStageLimit;
+            }
+            for (const auto& in : inputs) {
+                if (in.first == i_rows || !s.pieces[in.first].second) continue;
+                std::memcpy(ctx->stage + (s.pieces[in.first].first - rest0), in.second, s.pieces[in.first].second);
+            }
+            GD_CUDA(cudaMemcpyAsync(s.base + rest0, ctx->stage, rest, cudaMemcpyHostToDevice, ctx->stream),
+                    "H2D staged inputs");
+            GD_CUDA(cudaEventRecord(ctx->stage_ev, ctx->stream), "stage event record");
+        } else {
+            for (const auto& in : inputs) {
+                if (in.first == i_rows || !s.pieces[in.first].second) continue;
+                GD_CUDA(cudaMemcpyAsync(s.ptr(in.first), in.second, s.pieces[in.first].second, cudaMemcpyHostToDevice,
+                                        ctx->stream),
+                        "H2D grid input");
+            }
         }
     }
     gd_grid dg = *g;
