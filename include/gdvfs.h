@@ -11,7 +11,10 @@
  *
  * Threading: one gd_ctx per (device, host thread).  Calls that take host
  * buffers are synchronous; *_device variants take device pointers, enqueue on
- * the context's stream and return without synchronising.
+ * the context's stream and return without synchronising.  A context keeps
+ * grow-only device scratch, a pinned staging buffer and (for small
+ * decisions-only gd_grid_select calls) CUDA graphs of the whole call keyed by
+ * (models, batch shape, options, stream); GDVFS_GRAPHS=0 disables the graphs.
  */
 #ifndef GDVFS_H
 #define GDVFS_H
