@@ -8,6 +8,7 @@
 //   dadd_probe                         FP64 add-pipe peak for the roofline
 //
 // No tensor cores: tree traversal is not a contraction.
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "gd_common.cuh"
@@ -58,6 +59,85 @@ __global__ void __launch_bounds__(256) predict_gbt_kernel(const PNode* __restric
         if (lane == 0) {
             double y = finish(base, lr, acc);
             out[r] = clamp ? clamp_energy(y) : y;
+        }
+    }
+}
+
+// K1, rows on lanes: a warp takes 32 rows and every lane walks the SAME tree
+// for its own row, trees in model order (the in-order sum stays per lane).
+// Top levels are one broadcast load for the whole warp and only the deep
+// levels diverge, so each tree costs ~1/2 the L1 wavefronts of the
+// lanes-on-trees form above; rows sit transposed in shared memory
+// ([feature][lane]: conflict-free whatever feature each lane tests).  Two
+// trees per lane advance in lockstep for ILP.
+constexpr int kK1Warps = 4;
+#ifndef GD_K1_WALKS
+#define GD_K1_WALKS 2
+#endif
+constexpr int kK1Walks = GD_K1_WALKS;  // trees per lane in lockstep
+__global__ void __launch_bounds__(kK1Warps * 32) predict_gbt_rows_kernel(
+    const PNode* __restrict__ nodes, const int32_t* __restrict__ roots, int32_t n_trees, double base, double lr,
+    int clamp, const double* __restrict__ rows, int64_t n_rows, int32_t n_cols, double* __restrict__ out,
+    int32_t* __restrict__ leaf_ids) {
+    extern __shared__ double smem_rows[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* rt = smem_rows + static_cast<int64_t>(warp) * n_cols * 32;  // [feature][lane]
+    const int64_t n_blocks = (n_rows + 31) / 32;
+    for (int64_t rb = static_cast<int64_t>(blockIdx.x) * kK1Warps + warp; rb < n_blocks;
+         rb += static_cast<int64_t>(gridDim.x) * kK1Warps) {
+        const int64_t r0 = rb * 32;
+        const int nr = static_cast<int>(min(static_cast<int64_t>(32), n_rows - r0));
+        __syncwarp();
+        for (int i = lane; i < nr * n_cols; i += 32) {  // coalesced global, transposed shared
+            const int r = i / n_cols, f = i - r * n_cols;
+            rt[f * 32 + r] = __ldg(rows + r0 * n_cols + i);
+        }
+        __syncwarp();
+        const bool valid = lane < nr;
+        const double* myrow = rt + lane;  // feature f at myrow[32 f]
+        double acc = 0.0;
+        int32_t t = 0;
+        for (; t + kK1Walks <= n_trees; t += kK1Walks) {
+            int32_t n[kK1Walks], f[kK1Walks], aux[kK1Walks];
+            double v[kK1Walks];
+#pragma unroll
+            for (int h = 0; h < kK1Walks; ++h) {
+                n[h] = __ldg(roots + t + h);
+                load_node(nodes, n[h], v[h], f[h], aux[h]);
+            }
+            bool any = true;
+            while (any) {
+                any = false;
+#pragma unroll
+                for (int h = 0; h < kK1Walks; ++h) {
+                    if (f[h] >= 0) {
+                        n[h] = (myrow[32 * f[h]] <= v[h]) ? aux[h] : aux[h] + 1;
+                        load_node(nodes, n[h], v[h], f[h], aux[h]);
+                        any = true;
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < kK1Walks; ++h) {
+                acc = __dadd_rn(acc, v[h]);
+                if (leaf_ids && valid) leaf_ids[(r0 + lane) * n_trees + t + h] = aux[h];
+            }
+        }
+        for (; t < n_trees; ++t) {
+            int32_t n = __ldg(roots + t);
+            double v;
+            int32_t f, aux;
+            load_node(nodes, n, v, f, aux);
+            while (f >= 0) {
+                n = (myrow[32 * f] <= v) ? aux : aux + 1;
+                load_node(nodes, n, v, f, aux);
+            }
+            acc = __dadd_rn(acc, v);
+            if (leaf_ids && valid) leaf_ids[(r0 + lane) * n_trees + t] = aux;
+        }
+        if (valid) {
+            const double y = finish(base, lr, acc);
+            out[r0 + lane] = clamp ? clamp_energy(y) : y;
         }
     }
 }
@@ -299,17 +379,38 @@ int launch_select_cpl(const SelectParams& p, int sm_count, cudaStream_t stream) 
 int launch_predict_gbt(const PNode* nodes, const int32_t* roots, int32_t n_trees, double base, double lr, int clamp,
                        const double* rows, int64_t n_rows, int32_t n_cols, double* out, int32_t* leaf_ids,
                        int sm_count, void* stream) {
-    const int threads = 256;
-    const size_t smem = static_cast<size_t>(threads / 32) * n_cols * sizeof(double);
+    const char* env = std::getenv("GDVFS_K1_TREES_ON_LANES");
+    const size_t rows_smem = static_cast<size_t>(kK1Warps) * n_cols * 32 * sizeof(double);
+    // The lanes-on-trees form: for comparison, and for very wide rows whose
+    // 32-row transposed tile would not fit shared memory.
+    const bool few_rows = (n_rows + 31) / 32 < 4LL * sm_count * kK1Warps;  // too few 32-row tiles to fill the GPU
+    if ((env && env[0] == '1') || rows_smem > 200 * 1024 || (few_rows && !(env && env[0] == '0'))) {
+        const int threads = 256;
+        const size_t smem = static_cast<size_t>(threads / 32) * n_cols * sizeof(double);
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(predict_gbt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_gbt_kernel, threads, smem);
+        const int blocks = grid_blocks(threads / 32, n_rows, sm_count, per_sm);
+        predict_gbt_kernel<<<blocks, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+            nodes, roots, n_trees, base, lr, clamp, rows, n_rows, n_cols, out, leaf_ids);
+        return cudaGetLastError();
+    }
+    const size_t smem = rows_smem;
     if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(predict_gbt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(predict_gbt_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_gbt_kernel, threads, smem);
-    const int blocks = grid_blocks(threads / 32, n_rows, sm_count, per_sm);
-    predict_gbt_kernel<<<blocks, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_gbt_rows_kernel, kK1Warps * 32, smem);
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t n_blocks = (n_rows + 31) / 32;
+    const int blocks = grid_blocks(kK1Warps, n_blocks, sm_count, per_sm);
+    predict_gbt_rows_kernel<<<blocks, kK1Warps * 32, smem, static_cast<cudaStream_t>(stream)>>>(
         nodes, roots, n_trees, base, lr, clamp, rows, n_rows, n_cols, out, leaf_ids);
     return cudaGetLastError();
 }
