@@ -44,8 +44,13 @@ def test_k1_predict_matches_reference_golden(ctx, key):
     assert np.array_equal(ids, want_ids)
 
 
+@pytest.mark.parametrize("form", ["auto", "rows_on_lanes", "trees_on_lanes"])
 @pytest.mark.parametrize("leaf_prob,depth,trees", [(0.0, 8, 67), (0.35, 10, 40), (0.0, 1, 5), (0.2, 12, 33)])
-def test_k1_predict_leaf_ids_vs_oracle(ctx, leaf_prob, depth, trees):
+def test_k1_predict_leaf_ids_vs_oracle(ctx, leaf_prob, depth, trees, form, monkeypatch):
+    # both K1 forms (the library picks by batch size; forced here): 350 rows =
+    # 10 full 32-row tiles + a partial one; odd tree counts hit the lockstep tail
+    if form != "auto":
+        monkeypatch.setenv("GDVFS_K1_TREES_ON_LANES", "1" if form == "trees_on_lanes" else "0")
     sc = W.make_scenario("k1", 50, "gtx980", trees, depth, seed=depth, w_clk=0.1, leaf_prob=leaf_prob)
     rows = np.repeat(sc.grid.rows, 7, axis=0)
     rows[:, W.SM_COL] = np.resize(sc.grid.sm, rows.shape[0])
