@@ -869,13 +869,16 @@ struct RingT {
     __host__ __device__ static constexpr int rs(int g) { return g % (RR + 1); }  // record slot
     __host__ __device__ static constexpr int ss(int g) { return g % (RS + 1); }  // side slot
 };
-#ifndef GD_ACC_RING
-#define GD_ACC_RING 2, 1
+#ifndef GD_ACC_RR
+#define GD_ACC_RR 2
+#endif
+#ifndef GD_ACC_RS
+#define GD_ACC_RS 1
 #endif
 #ifndef GD_SLICED_RING
 #define GD_SLICED_RING 8, 4
 #endif
-using AccRing = RingT<GD_ACC_RING>;        // main kernel (shared memory bound)
+using AccRing = RingT<GD_ACC_RR, GD_ACC_RS>;  // main kernel (shared memory bound)
 using SlicedRing = RingT<GD_SLICED_RING>;  // latency mode (few warps: deep prefetch)
 template <class RG>
 __host__ __device__ constexpr size_t acc_smem_per_warp(int n_cols) {
