@@ -853,7 +853,10 @@ constexpr int kAccThreads = kAccWarps * 32;
 // one cp.async commit group per iteration; an iteration waits only for the
 // group that carries its own side data and the records the next side fetch
 // reads, so kWait younger groups stay in flight.
-constexpr int kSide = 8;
+#ifndef GD_SIDE_SLOTS
+#define GD_SIDE_SLOTS 8
+#endif
+constexpr int kSide = GD_SIDE_SLOTS;  // residue tables staged per group (more: copied on demand)
 template <int RR, int RS>
 struct RingT {
     static_assert(RS >= 1 && RR > RS, "records must run ahead of the side data");
