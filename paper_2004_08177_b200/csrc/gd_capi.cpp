@@ -812,7 +812,16 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
                                                      {i_sm, g->sm_clock},      {i_mem, g->mem_clock},
                                                      {i_bud, g->budgets}};
     if (graphable && ctx->stage) {
-        if (gd_graph_entry* hit = find_graph(ctx, key)) {
+        gd_graph_entry* hit = find_graph(ctx, key);
+        // The graph holds the models' grid nodes as recoded for its clock
+        // columns; a call with other columns in between rebuilt them in place.
+        if (hit && (me->grid_sm_col != g->sm_col || me->grid_mem_col != g->mem_col || mt->grid_sm_col != g->sm_col ||
+                    mt->grid_mem_col != g->mem_col)) {
+            cudaGraphExecDestroy(hit->exec);
+            ctx->graphs.erase(ctx->graphs.begin() + (hit - ctx->graphs.data()));
+            hit = nullptr;
+        }
+        if (hit) {
             GD_CUDA(cudaEventSynchronize(ctx->stage_ev), "stage reuse");
             for (const auto& in : inputs) {
                 if (s.pieces[in.first].second) std::memcpy(ctx->stage + s.pieces[in.first].first, in.second, s.pieces[in.first].second);

@@ -152,6 +152,16 @@ def test_k2_graph_replay_stream_vs_oracle(ctx):
                             g.cat_cols.astype(np.int32), g.sm.astype(np.int32), g.mem.astype(np.int32), g.sm_col,
                             g.mem_col), np.ascontiguousarray(budgets[lo:lo + n])
 
+    # clock columns switched between two calls of one shape: the models' grid
+    # nodes are recoded in place, so a graph captured for the first columns
+    # must not be replayed for them afterwards
+    me0, mt0 = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    gw, bw = window(0, 64)
+    swapped = W.GridInputs(gw.rows, gw.cat_t, gw.cat_cols, gw.sm, gw.mem, g.mem_col, g.sm_col)
+    for grid_in in (gw, gw, swapped, gw, swapped, gw):
+        got = gd.grid_select(me0, mt0, grid_in, bw, opts_of(0, 1, 0, 0))
+        want, _, _ = O.oracle_grid(sc.energy, sc.time, grid_in, bw, 0, 0, 0)
+        assert decisions_equal(got, want)
     other = W.make_scenario("replay2", 8, "gtx980", 45, 7, seed=77, w_clk=0.1)
     for pair in range(2):
         f_e, f_t = (sc.energy, sc.time) if pair == 0 else (other.energy, other.time)
