@@ -178,7 +178,9 @@ def test_k2_graph_replay_stream_vs_oracle(ctx):
 @pytest.mark.parametrize("seed", range(64))
 def test_k2_fuzz_catalogs_and_shapes_vs_oracle(ctx, seed):
     """Random catalogs (any size up to 512, 1..40 memory clocks, arbitrary
-    order or the reference's (mem, sm) order, duplicate pairs allowed),
+    order or the reference's (mem, sm) order, duplicate pairs allowed -- the
+    reference only ever sees unique sorted catalogs; for the others the
+    oracle's per-index semantics are the contract),
     random tree shapes / clock-split rates, batch sizes on both sides of the
     latency-mode switch, random selection options: predictions and decisions
     bit-identical to the oracle, with and without the E/T tables (the

@@ -136,3 +136,46 @@ def test_oracle_edf_ties_live():
         want, wo = O.ref_schedule(jobs, E, T, X, sm, mem, mode, budget, obj, be)
         got, go = O.oracle_schedule(jobs, E, T, X, sm, mode, budget, obj, be)
         assert decisions_equal(got, want) and np.array_equal(go, wo)
+
+
+@needs_ref
+@pytest.mark.parametrize("seed", range(12))
+def test_oracle_fuzz_live_reference(seed):
+    """Random ensembles (depth, irregularity, clock-split rate), rows with NaN
+    and extreme feature values, and random E/T tables with heavy ties through
+    every selection option: the oracle and the reference's own compiled code
+    agree bit for bit."""
+    rng = np.random.default_rng(500 + seed)
+    sc = W.make_scenario("fz", 12, "gtx980", int(rng.integers(1, 40)), int(rng.integers(1, 11)), seed=seed,
+                         w_clk=float(rng.choice([0.0, 0.1, 0.4])), leaf_prob=float(rng.choice([0.0, 0.3])))
+    rows = np.repeat(sc.grid.rows, 4, axis=0)
+    rows[:, W.SM_COL] = np.resize(sc.grid.sm, rows.shape[0])
+    rows[:, W.MEM_COL] = np.resize(sc.grid.mem, rows.shape[0])
+    mask = rng.random(rows.shape) < 0.05
+    rows[mask] = np.nan
+    rows[rng.random(rows.shape) < 0.02] = 1e300
+    rows[rng.random(rows.shape) < 0.02] = -1e300
+    for f in (sc.energy, sc.time):
+        assert np.array_equal(bits(O.oracle_predict(f, rows)), bits(O.ref_predict(f, rows)))
+    # selection + EDF over tie-heavy tables
+    n, A, Cn = 40, 9, int(rng.integers(1, 20))
+    jobs = np.zeros(n, O.JOB_DTYPE)
+    jobs["arrival_s"] = rng.integers(0, 6, size=n).astype(np.float64)
+    jobs["deadline_s"] = rng.integers(1, 5, size=n).astype(np.float64)
+    jobs["app_rank"] = rng.permutation(n)
+    jobs["app_index"] = rng.integers(0, A, size=n)
+    E = rng.integers(1, 4, size=(A, Cn)).astype(np.float64)
+    T = rng.integers(1, 5, size=(A, Cn)).astype(np.float64) * 0.5
+    X = T * rng.choice([0.5, 1.0, 1.5], size=(A, Cn))
+    # a valid catalog: unique (sm, mem) pairs in clock_catalog order (mem, sm ascending)
+    pairs = sorted({(int(m), int(x)) for m, x in zip(rng.choice([405, 810, 3505], size=Cn),
+                                                     rng.integers(300, 1500, size=Cn))})
+    Cn = len(pairs)
+    E, T, X = E[:, :Cn], T[:, :Cn], X[:, :Cn]
+    sm = np.array([x for _, x in pairs], np.int32)
+    mem = np.array([m for m, _ in pairs], np.int32)
+    for mode, budget, obj, be in itertools.product((0, 1), repeat=4):
+        want, worder = O.ref_schedule(jobs, E, T, X, sm, mem, mode, budget, obj, be)
+        got, gorder = O.oracle_schedule(jobs, E, T, X, sm, mode, budget, obj, be)
+        assert decisions_equal(got, want), (seed, mode, budget, obj, be)
+        assert np.array_equal(gorder, worder)
