@@ -197,6 +197,10 @@ def test_k2_fuzz_catalogs_and_shapes_vs_oracle(ctx, seed):
     n_apps = int(rng.choice([1, 7, 64, 255, 257, 600]))
     sc = W.make_scenario("fuzz", n_apps, (sm, mem), int(rng.integers(1, 80)), int(rng.integers(1, 11)), seed=seed,
                          w_clk=float(rng.choice([0.0, 0.05, 0.2, 0.5])), leaf_prob=float(rng.choice([0.0, 0.3])))
+    if rng.random() < 0.5:  # NaN / extreme feature values (clock columns are substituted anyway)
+        rows = sc.grid.rows
+        rows[rng.random(rows.shape) < 0.03] = np.nan
+        rows[rng.random(rows.shape) < 0.01] = 1e300
     me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
     _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(n_apps))
     budgets = W.deadlines_from_times(t0, seed=seed)
