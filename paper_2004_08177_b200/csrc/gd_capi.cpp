@@ -712,19 +712,32 @@ gd_graph_entry* find_graph(gd_ctx* ctx, const gd_graph_entry& key) {
 void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& dg, const gd_select_opts& o,
                    gd_graph_entry key, void* dev_in, size_t in_end, gd_decision* dev_out) {
     const size_t out_bytes = static_cast<size_t>(dg.n_apps) * sizeof(gd_decision);
-    if (!ctx->out_stage && cudaHostAlloc(reinterpret_cast<void**>(&ctx->out_stage), kStageLimit, cudaHostAllocDefault) !=
+    if (!ctx->out_stage && cudaHostAlloc(reinterpret_cast<void**>(&ctx->out_stage), kStageLimit, cudaHostAllocMapped) !=
                                cudaSuccess) {
         ctx->out_stage = nullptr;
         cudaGetLastError();
         return;
+    }
+    // Decisions go straight from the selection epilogue into the mapped
+    // pinned staging (24 B per app over the bus) instead of a device buffer
+    // plus a copy node (GDVFS_GRAPH_D2H=1 keeps the copy).
+    gd_decision* host_out = nullptr;
+    const char* d2h = std::getenv("GDVFS_GRAPH_D2H");
+    if (!(d2h && d2h[0] == '1') &&
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&host_out), ctx->out_stage, 0) != cudaSuccess) {
+        host_out = nullptr;
+        cudaGetLastError();
     }
     const int64_t launches = ctx->launches;
     cudaGraph_t graph = nullptr;
     bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
         ok = cudaMemcpyAsync(dev_in, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
-        ok = ok && grid_impl(ctx, me, mt, dg, o, dev_out, nullptr, nullptr, nullptr, false) == GD_OK;
-        ok = ok && cudaMemcpyAsync(ctx->out_stage, dev_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
+        ok = ok && grid_impl(ctx, me, mt, dg, o, host_out ? host_out : dev_out, nullptr, nullptr, nullptr, false) == GD_OK;
+        if (!host_out) {
+            ok = ok &&
+                 cudaMemcpyAsync(ctx->out_stage, dev_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
+        }
         ok = (cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess) && ok;
     }
     ctx->launches = launches;
