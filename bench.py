@@ -287,6 +287,11 @@ def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_
         stats = torch.cat([mx, tot])
     step_ms, kern_ms, launches = (float(x) for x in stats.cpu())
 
+    # The clock sampler covered the device-timed steps; it stops here so its
+    # nvidia-smi queries (every 100 ms, they take the driver lock) cannot land
+    # inside the host-API timings below.
+    clocks = sampler.stop() if sampler is not None else None
+
     # e2e: the public host-buffer API (pinned inputs H2D + kernel + D2H decisions).
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     h_grid = W.GridInputs(pin(g.rows[lo:hi]), pin(g.cat_t[lo:hi]), pin(g.cat_cols.astype(np.int32)),
@@ -307,6 +312,8 @@ def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_
         gd.grid_select(me, mt, h_grid, h_bud, opts, out=h_out)
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
+    e2e_p50 = float(np.median(e2e_times))
+    e2e_max = float(np.max(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -324,7 +331,6 @@ def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_
     ctx.set_timing(False)
     kernels_ms = {k: float(np.sum(v) / args.steps) for k, v in kern.items()}
     c5 = c5_latency(me, mt, h_grid, h_bud, opts, A) if rank == 0 else None
-    clocks = sampler.stop() if sampler is not None else None
 
     # Consistency: the device-resident run and the e2e run agree.
     dev_dec = out_d.cpu().numpy().view(gd.DECISION_DTYPE)
@@ -371,6 +377,7 @@ def _timed(args, rank, world, dev, stream, ctx, me, mt, g, sc, cfg, per_rank, n_
             "e2e": {"value": units_total / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(A * (F + K + 1) * 8 + K * 4 + C_ * 8),
                     "d2h_bytes_per_step": int(A * shard.DECISION_BYTES), "ms_per_step": e2e_s * 1e3,
+                    "ms_p50": e2e_p50 * 1e3, "ms_max": e2e_max * 1e3,
                     "api": "gd_grid_select (C ABI, pinned host buffers)"},
             "gpu_launches": int(launches),
             "wall_ms_per_step_incl_l2_flush": wall / args.steps * 1e3,
