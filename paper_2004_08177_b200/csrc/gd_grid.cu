@@ -843,7 +843,10 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
 #define GD_ACC_MIN_BLOCKS 6
 #endif
 constexpr int64_t kRankWarpLimit = 1 << 16;  // ranks per batch below which a warp takes each
-constexpr int kAccWarps = 4;  // 2 warp pairs = 2 apps in flight per CTA
+#ifndef GD_ACC_WARPS
+#define GD_ACC_WARPS 4
+#endif
+constexpr int kAccWarps = GD_ACC_WARPS;  // 2 warp pairs = 2 apps in flight per CTA
 constexpr int kAccThreads = kAccWarps * 32;
 
 // Per-warp shared region of the two-stage prefetch ring: record slots
@@ -1269,13 +1272,22 @@ __device__ __forceinline__ void pair_sync() {
     asm volatile("barrier.sync %0, 64;" ::"n"(kId) : "memory");
 }
 __device__ __forceinline__ void pair_sync_a(int pair) {
-    if (pair == 0) pair_sync<1>();
-    else pair_sync<3>();
+    switch (pair) {
+        case 0: pair_sync<1>(); break;
+        case 1: pair_sync<3>(); break;
+        case 2: pair_sync<5>(); break;
+        default: pair_sync<7>(); break;
+    }
 }
 __device__ __forceinline__ void pair_sync_b(int pair) {
-    if (pair == 0) pair_sync<2>();
-    else pair_sync<4>();
+    switch (pair) {
+        case 0: pair_sync<2>(); break;
+        case 1: pair_sync<4>(); break;
+        case 2: pair_sync<6>(); break;
+        default: pair_sync<8>(); break;
+    }
 }
+static_assert(kAccWarps / 2 <= 4, "pair barriers cover four warp pairs");
 
 // The catalog -> (lane, slot) map, built by one warp into map[slot * 32 +
 // lane] (catalog index or -1).  Preferred: every lane's clocks lie in ONE run
