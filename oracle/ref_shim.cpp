@@ -465,7 +465,8 @@ int ref_truth_oracle(uint64_t seed_offset, const double* deadlines, double* ener
 double ref_bench_grid(const ForestView* fe, double base_e, double lr_e, const ForestView* ft, double base_t,
                       double lr_t, const double* rows, int n_cols, const double* cat_t, const int32_t* cat_cols,
                       int n_cat, int64_t n_apps, const int32_t* sm, const int32_t* mem, int32_t n_clocks, int sm_col,
-                      int mem_col, const double* budgets, int threads, Decision* out) {
+                      int mem_col, const double* budgets, int threads, Decision* out, double* e_out,
+                      double* t_out) {
     try {
         models::FittedModel me = forest_model(fe, base_e, lr_e, 0, n_cols);
         models::FittedModel mt = forest_model(ft, base_t, lr_t, 1, n_cols);
@@ -492,6 +493,8 @@ double ref_bench_grid(const ForestView* fe, double base_e, double lr_e, const Fo
                         }
                         std::vector<double> e = models::predict(me, xe);
                         std::vector<double> t = models::predict(mt, xt);
+                        if (e_out) std::copy(e.begin(), e.end(), e_out + a * n_clocks);
+                        if (t_out) std::copy(t.begin(), t.end(), t_out + a * n_clocks);
                         DeviceSpec dev;
                         dev.name = "bench";
                         for (int c = 0; c < n_clocks; ++c) dev.supported_clocks.push_back({sm[c], mem[c]});

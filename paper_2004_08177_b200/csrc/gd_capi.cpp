@@ -687,7 +687,7 @@ bool graphs_enabled() {
 }
 
 bool same_key(const gd_graph_entry& a, const gd_graph_entry& b) {
-    return a.me == b.me && a.mt == b.mt && a.n_apps == b.n_apps && a.n_clocks == b.n_clocks && a.n_cols == b.n_cols &&
+    return a.me == b.me && a.mt == b.mt && a.n_apps == b.n_apps && a.n_records == b.n_records && a.n_clocks == b.n_clocks && a.n_cols == b.n_cols &&
            a.n_cat == b.n_cat && a.sm_col == b.sm_col && a.mem_col == b.mem_col && a.mode == b.mode &&
            a.objective == b.objective && a.best_effort == b.best_effort && a.stream == b.stream;
 }
@@ -811,6 +811,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     key.me = me->uid;
     key.mt = mt->uid;
     key.n_apps = A;
+    key.n_records = R;
     key.n_clocks = static_cast<int32_t>(C);
     key.n_cols = g->n_cols;
     key.n_cat = g->n_cat;

@@ -26,6 +26,7 @@ struct gd_pbuf {
 struct gd_graph_entry {
     uint64_t me = 0, mt = 0;  // model uids
     int64_t n_apps = 0;
+    int64_t n_records = 0;  // staged piece offsets (cat_t .. budgets) depend on it
     int32_t n_clocks = 0, n_cols = 0, n_cat = 0, sm_col = 0, mem_col = 0;
     int32_t mode = 0, objective = 0, best_effort = 0;
     cudaStream_t stream = nullptr;

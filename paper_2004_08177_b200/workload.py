@@ -255,6 +255,57 @@ def make_rows(cols: _ColumnModel, n_apps: int, seed: int, sm_default: int, mem_d
     return np.ascontiguousarray(rows), np.ascontiguousarray(cat_t)
 
 
+CHUNK_APPS = 1 << 16  # apps per independently seeded chunk (large configs)
+
+
+def _rows_chunk(cols: _ColumnModel, seed: int, chunk: int, sm_default: int, mem_default: int):
+    return make_rows(cols, CHUNK_APPS, hash_seed(seed, 0x524f5753, chunk), sm_default, mem_default)
+
+
+def make_rows_range(cols: _ColumnModel, lo: int, hi: int, seed: int, sm_default: int, mem_default: int,
+                    threads: int = 0):
+    """Rows of apps [lo, hi) of a chunk-seeded scenario: chunk k (apps
+    [k*CHUNK_APPS, (k+1)*CHUNK_APPS)) draws from its own seed, so any app
+    range -- one rank's shard of configs[3]'s 10M apps, or the reference
+    arm's sample -- is generated alone and matches the whole batch's rows."""
+    n = hi - lo
+    rows = np.empty((n, cols.n_cols), np.float64)
+    cat_t = np.empty((n, len(cols.cat_cols)), np.float64)
+    if n <= 0:
+        return rows, cat_t
+    k0, k1 = lo // CHUNK_APPS, (hi - 1) // CHUNK_APPS
+
+    def one(k):
+        r, c = _rows_chunk(cols, seed, k, sm_default, mem_default)
+        a, b = max(lo, k * CHUNK_APPS), min(hi, (k + 1) * CHUNK_APPS)
+        rows[a - lo:b - lo] = r[a - k * CHUNK_APPS:b - k * CHUNK_APPS]
+        cat_t[a - lo:b - lo] = c[a - k * CHUNK_APPS:b - k * CHUNK_APPS]
+
+    ks = range(k0, k1 + 1)
+    if threads != 1 and len(ks) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        with ThreadPoolExecutor(threads or min(16, os.cpu_count() or 1)) as ex:
+            list(ex.map(one, ks))
+    else:
+        for k in ks:
+            one(k)
+    return rows, cat_t
+
+
+def hash_seed(*parts: int) -> int:
+    """SplitMix64 over the parts (a counter-based seed: chunk k of seed s is
+    the same whatever else is generated)."""
+    x = 0
+    for p in parts:
+        x = (x + 0x9E3779B97F4A7C15 + (int(p) & 0xFFFFFFFFFFFFFFFF)) & 0xFFFFFFFFFFFFFFFF
+        z = x
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        x = z ^ (z >> 31)
+    return x
+
+
 @dataclasses.dataclass
 class Scenario:
     name: str
@@ -262,13 +313,26 @@ class Scenario:
     time: Forest
     grid: GridInputs
     seed: int
+    cols: Optional[_ColumnModel] = None
+    app_range: tuple = (0, 0)  # global indices of grid's apps (chunked scenarios)
+
+    def rows_range(self, lo: int, hi: int):
+        """Rows + time-encoded categorical values of global apps [lo, hi)
+        (chunk-seeded scenarios only)."""
+        sm, mem = self.grid.sm, self.grid.mem
+        return make_rows_range(self.cols, lo, hi, self.seed + 3, int(sm[-1]), int(mem[-1]))
 
 
 def make_scenario(name: str, n_apps: int, catalog, n_trees: int, depth: int, seed: int = 1234,
-                  w_clk: float = 0.04, leaf_prob: float = 0.0) -> Scenario:
+                  w_clk: float = 0.04, leaf_prob: float = 0.0, chunked: Optional[bool] = None,
+                  app_range: Optional[tuple] = None) -> Scenario:
     """A complete synthetic (apps, catalog, E/T ensembles) configuration.
     `catalog`: a CATALOGS name or an explicit (sm, mem) pair of int32 arrays
-    in the order the candidates are to be evaluated (any order)."""
+    in the order the candidates are to be evaluated (any order).
+
+    Batches above CHUNK_APPS apps (configs[2] / configs[3]) draw their rows
+    chunk by chunk (`make_rows_range`); `app_range=(lo, hi)` then builds only
+    those apps of the n_apps-app batch (one rank's shard, a CPU sample)."""
     if isinstance(catalog, str):
         sm, mem = CATALOGS[catalog]()
     else:
@@ -277,9 +341,15 @@ def make_scenario(name: str, n_apps: int, catalog, n_trees: int, depth: int, see
     cols = _ColumnModel(rng, N_COLS, CAT_COLS, sm, mem, SM_COL, MEM_COL)
     fe = make_forest(cols, n_trees, depth, 0, seed + 1, w_clk, leaf_prob)
     ft = make_forest(cols, n_trees, depth, 1, seed + 2, w_clk, leaf_prob)
-    rows, cat_t = make_rows(cols, n_apps, seed + 3, int(sm[-1]), int(mem[-1]))
+    if chunked is None:
+        chunked = n_apps > CHUNK_APPS or app_range is not None
+    lo, hi = app_range if app_range is not None else (0, n_apps)
+    if chunked:
+        rows, cat_t = make_rows_range(cols, lo, hi, seed + 3, int(sm[-1]), int(mem[-1]))
+    else:
+        rows, cat_t = make_rows(cols, n_apps, seed + 3, int(sm[-1]), int(mem[-1]))
     grid = GridInputs(rows, cat_t, np.array(CAT_COLS, dtype=np.int32), sm, mem, SM_COL, MEM_COL)
-    return Scenario(name, fe, ft, grid, seed)
+    return Scenario(name, fe, ft, grid, seed, cols, (lo, hi))
 
 
 def deadlines_from_times(times: np.ndarray, seed: int, infeasible_frac: float = 0.05) -> np.ndarray:
@@ -293,6 +363,38 @@ def deadlines_from_times(times: np.ndarray, seed: int, infeasible_frac: float = 
     idx = np.minimum((q * (times.shape[1] - 1)).astype(np.int64), times.shape[1] - 1)
     dl = srt[np.arange(a), idx].copy()
     bad = rng.random(size=a) < infeasible_frac
+    dl[bad] = srt[bad, 0] * 0.5
+    return dl
+
+
+def deadline_draws(seed: int, lo: int, hi: int, infeasible_frac: float = 0.05):
+    """Per-app deadline draws of `deadlines_from_times` for global apps
+    [lo, hi), chunk-seeded like the rows: the quantile q ~ U(0.1, 0.9) and the
+    `bad` flag (deadline = half the minimum time) of app i are the same in
+    any app range, so the reference arm's sample and every rank's shard see
+    the deadlines of the whole batch."""
+    n = max(hi - lo, 0)
+    q = np.empty(n)
+    bad = np.empty(n, bool)
+    if n == 0:
+        return q, bad
+    for k in range(lo // CHUNK_APPS, (hi - 1) // CHUNK_APPS + 1):
+        r = np.random.default_rng(hash_seed(seed, 0x444c, k))
+        qk = r.uniform(0.1, 0.9, size=CHUNK_APPS)
+        bk = r.random(size=CHUNK_APPS) < infeasible_frac
+        a, b = max(lo, k * CHUNK_APPS), min(hi, (k + 1) * CHUNK_APPS)
+        q[a - lo:b - lo] = qk[a - k * CHUNK_APPS:b - k * CHUNK_APPS]
+        bad[a - lo:b - lo] = bk[a - k * CHUNK_APPS:b - k * CHUNK_APPS]
+    return q, bad
+
+
+def deadlines_from_draws(times: np.ndarray, q: np.ndarray, bad: np.ndarray) -> np.ndarray:
+    """The deadlines_from_times rule for given draws (numpy; bench.py runs the
+    same rule on device tensors)."""
+    srt = np.sort(times, axis=1)
+    c = times.shape[1]
+    idx = np.minimum((q * (c - 1)).astype(np.int64), c - 1)
+    dl = srt[np.arange(times.shape[0]), idx].copy()
     dl[bad] = srt[bad, 0] * 0.5
     return dl
 

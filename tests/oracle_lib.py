@@ -101,7 +101,7 @@ def ref() -> Optional[C.CDLL]:
         r.ref_bench_grid.restype = C.c_double
         r.ref_bench_grid.argtypes = [C.POINTER(ForestView), C.c_double, C.c_double, C.POINTER(ForestView),
                                      C.c_double, C.c_double, P, C.c_int, P, P, C.c_int, C.c_int64, P, P, C.c_int32,
-                                     C.c_int, C.c_int, P, C.c_int, P]
+                                     C.c_int, C.c_int, P, C.c_int, P, P, P]
         _ref = r
     return _ref
 
@@ -266,7 +266,10 @@ def ref_truth_oracle(seed_offset, deadlines):
     return E, T, out, sm
 
 
-def ref_bench_grid(fe, ft, grid, budgets, n_apps, threads):
+def ref_bench_grid(fe, ft, grid, budgets, n_apps, threads, tables=False):
+    """The reference's predict (E, T over materialised candidate rows) +
+    schedule_d_dvfs(full_deadline) per app on `threads` host threads; returns
+    (seconds, decisions) or, with ``tables``, (seconds, decisions, E, T)."""
     fve, k1 = forest_view(fe)
     fvt, k2 = forest_view(ft)
     rows = np.ascontiguousarray(grid.rows[:n_apps], np.float64)
@@ -276,9 +279,22 @@ def ref_bench_grid(fe, ft, grid, budgets, n_apps, threads):
     mem = np.ascontiguousarray(grid.mem, np.int32)
     b = np.ascontiguousarray(budgets[:n_apps], np.float64)
     out = np.zeros(n_apps, DECISION_DTYPE)
+    E = np.empty((n_apps, sm.shape[0])) if tables else None
+    T = np.empty((n_apps, sm.shape[0])) if tables else None
     secs = ref().ref_bench_grid(C.byref(fve), fe.base, fe.learning_rate, C.byref(fvt), ft.base, ft.learning_rate,
                                 _p(rows), rows.shape[1], _p(cat_t), _p(cat_cols), cat_cols.shape[0], n_apps, _p(sm),
-                                _p(mem), sm.shape[0], grid.sm_col, grid.mem_col, _p(b), threads, _p(out))
+                                _p(mem), sm.shape[0], grid.sm_col, grid.mem_col, _p(b), threads, _p(out), _p(E),
+                                _p(T))
     if secs < 0:
         raise RuntimeError(ref().ref_last_error().decode())
-    return secs, out
+    return (secs, out, E, T) if tables else (secs, out)
+
+
+def ref_grid_tables(fe, ft, grid, threads=0):
+    """E/T candidate tables of every app of `grid` from the reference's own
+    predict (record = app; untimed use: deadlines for a CPU sample)."""
+    import os
+
+    n = grid.n_apps
+    _, dec, E, T = ref_bench_grid(fe, ft, grid, np.ones(n), n, threads or (os.cpu_count() or 1), tables=True)
+    return dec, E, T

@@ -175,6 +175,36 @@ def test_k2_graph_replay_stream_vs_oracle(ctx):
                 assert decisions_equal(got, want), (pair, combo, k)
 
 
+def test_k2_graph_replay_n_records_change(ctx):
+    """With rec_of_clock NULL the ABI allows n_records >= n_apps (record =
+    app); the staged offsets of cat_t .. budgets depend on n_records, so a
+    graph captured at one n_records must not be replayed at another (the
+    replay key includes it).  Alternates R = A and R > A at the same A."""
+    import ctypes as C
+
+    from paper_2004_08177_b200 import _capi
+    sc = W.make_scenario("nrec", 200, "gtx980", 40, 8, seed=41, w_clk=0.08)
+    g = sc.grid
+    A = 64
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, g, np.ones(g.n_apps))
+    budgets = np.ascontiguousarray(W.deadlines_from_times(t0, seed=4)[:A])
+    sub = W.GridInputs(np.ascontiguousarray(g.rows[:A]), np.ascontiguousarray(g.cat_t[:A]), g.cat_cols, g.sm, g.mem,
+                       g.sm_col, g.mem_col)
+    want, _, _ = O.oracle_grid(sc.energy, sc.time, sub, budgets, 0, 0, 0)
+    cat_cols, sm, mem = (np.ascontiguousarray(x, np.int32) for x in (g.cat_cols, g.sm, g.mem))
+    opts = opts_of(0, 1, 0, 0).opts()
+    for R in (A, 100, A, A, 150, 150, A, 100):
+        rows = np.ascontiguousarray(g.rows[:R])
+        cat = np.ascontiguousarray(g.cat_t[:R])
+        gs = _capi.Grid(gd._ptr(rows), R, rows.shape[1], cat.shape[1], gd._ptr(cat), gd._ptr(cat_cols), None, A,
+                        gd._ptr(sm), gd._ptr(mem), sm.shape[0], g.sm_col, g.mem_col, 0, gd._ptr(budgets))
+        out = np.zeros(A, gd.DECISION_DTYPE)
+        gd._raise(_capi.lib().gd_grid_select(ctx.handle, me.handle, mt.handle, C.byref(gs), C.byref(opts),
+                                             gd._ptr(out), None, None))
+        assert decisions_equal(out, want), R
+
+
 @pytest.mark.parametrize("seed", range(64))
 def test_k2_fuzz_catalogs_and_shapes_vs_oracle(ctx, seed):
     """Random catalogs (any size up to 512, 1..40 memory clocks, arbitrary
