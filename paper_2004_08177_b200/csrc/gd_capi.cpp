@@ -155,6 +155,17 @@ int upload_model(gd_model* m) {
         }
         for (size_t t = 0; t + 1 < roots.size(); ++t) wroots.push_back(wroots.back() + ((roots[t + 1] - roots[t] + 1) & ~1));
         m->n_wnodes = wroots.back();
+        std::vector<int32_t> wint;
+        m->max_wint = 0;
+        for (size_t t = 0; t + 1 < roots.size(); ++t) {
+            int32_t last = -1;
+            for (int32_t i = roots[t]; i < roots[t + 1]; ++i) {
+                if (nodes[static_cast<size_t>(i)].feat >= 0) last = i - roots[t];
+            }
+            const int32_t w = ((last + 1) + 1) & ~1;
+            wint.push_back(w < 2 ? 2 : w);
+            if (wint.back() > m->max_wint) m->max_wint = wint.back();
+        }
         if (!m->ctx) return GD_OK;  // host-only model: validated, never uploaded
         if (!thr.empty()) {
             GD_CUDA(cudaMalloc(&m->d_thr, thr.size() * sizeof(double)), "cudaMalloc(thresholds)");
@@ -164,6 +175,11 @@ int upload_model(gd_model* m) {
         GD_CUDA(cudaMalloc(&m->d_thr_off, thr_off.size() * sizeof(int32_t)), "cudaMalloc(threshold offsets)");
         GD_CUDA(cudaMemcpy(m->d_thr_off, thr_off.data(), thr_off.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
                 "cudaMemcpy(threshold offsets)");
+        if (!wint.empty()) {
+            GD_CUDA(cudaMalloc(&m->d_wint, wint.size() * sizeof(int32_t)), "cudaMalloc(walk prefixes)");
+            GD_CUDA(cudaMemcpy(m->d_wint, wint.data(), wint.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+                    "cudaMemcpy(walk prefixes)");
+        }
         GD_CUDA(cudaMalloc(&m->d_wroots, wroots.size() * sizeof(int32_t)), "cudaMalloc(walk roots)");
         GD_CUDA(cudaMemcpy(m->d_wroots, wroots.data(), wroots.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
                 "cudaMemcpy(walk roots)");
@@ -195,6 +211,8 @@ void release_model(gd_model* m) {
     if (m->d_thr) cudaFree(m->d_thr);
     if (m->d_thr_off) cudaFree(m->d_thr_off);
     if (m->d_wroots) cudaFree(m->d_wroots);
+    if (m->d_wint) cudaFree(m->d_wint);
+    m->d_wint = nullptr;
     m->d_thr = nullptr;
     m->d_thr_off = nullptr;
     m->d_wroots = nullptr;
@@ -336,6 +354,9 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.t_wnodes = mt->d_wnodes;
     p.e_wroots = me->d_wroots;
     p.t_wroots = mt->d_wroots;
+    p.e_wint = me->d_wint;
+    p.t_wint = mt->d_wint;
+    p.max_wint = me->max_wint > mt->max_wint ? me->max_wint : mt->max_wint;
     p.e_thr = me->d_thr;
     p.t_thr = mt->d_thr;
     p.e_thr_off = me->d_thr_off;

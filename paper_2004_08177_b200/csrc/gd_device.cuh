@@ -28,9 +28,11 @@ static_assert(sizeof(PNode) == 16, "PNode must stay 16 bytes");
 //             thresholds of its feature (-1 for a NaN threshold);
 //   clock:    key = t16 (clamp(floor(thr), 0, 65535));
 //   leaf:     key = packed (grid) index of the leaf;
-//   fc = feat << 19 | 8 * child: feat (signed; kFeat* for leaf / clock) in
-//   the top 13 bits, the byte offset of the left child within its tree (right
-//   = +8) in the low 19 bits.  With rank(x) = #{thresholds of the feature < x} (NaN x:
+//   fc = feat << 19 | 8 * child | leaf flags: feat (signed; kFeat* for leaf /
+//   clock) in the top 13 bits, the byte offset of the left child within its
+//   tree (right = +8) in the low 19 bits, whose 3 low bits are free: bit 0 set
+//   when the left child is a leaf, bit 1 when the right one is (a walk stops
+//   at the parent; the leaf's packed index is the tree's root + its position).  With rank(x) = #{thresholds of the feature < x} (NaN x:
 //   their count), `x <= thr_k  <=>  rank(x) <= k` exactly.
 struct __align__(8) WNode {
     int32_t key;
@@ -62,6 +64,9 @@ struct GridParams {
     int32_t e_trees, t_trees;
     int32_t e_max_pair_nodes, t_max_pair_nodes;  // roots[] carry a sentinel roots[n_trees]
     int32_t max_tree_nodes;
+    const int32_t* e_wint;  // per tree: loadable walk-node prefix (up to the last internal node, even)
+    const int32_t* t_wint;
+    int32_t max_wint;
     int32_t rank16;  // every feature has <= 65535 distinct thresholds (16-bit ranks)
 
     const double* rows;    // [n_records, n_cols] energy-encoded

@@ -133,6 +133,7 @@ struct WalkParams {
     const WNode* wnodes[2];
     const int32_t* wroots[2];  // n_trees + 1 entries, walk-node units
     const int32_t* roots[2];   // grid roots, n_trees + 1 entries
+    const int32_t* wint[2];    // per tree: loadable walk-node prefix (window size when it fits)
     const PNode* gnodes[2];    // grid nodes (leaf values)
     int32_t n_trees[2];
     const uint16_t* ranks;     // [2][n_apps][n_cols] for the batch
@@ -171,7 +172,9 @@ struct Walk {
 };
 
 __device__ __forceinline__ int32_t wfeat(int32_t fc) { return fc >> 19; }
-__device__ __forceinline__ int32_t wchild(int32_t fc) { return fc & 0x7ffff; }  // byte offset of the left child
+__device__ __forceinline__ int32_t wchild(int32_t fc) { return fc & 0x7fff8; }  // byte offset of the left child
+// fc of a leaf synthesized from its parent's flags (feat = kFeatLeaf).
+constexpr int32_t kLeafFc = static_cast<int32_t>(0xfff80000u);
 
 // Where one tree's walk nodes live during a stage.
 struct TreeSrc {
@@ -208,15 +211,17 @@ __device__ __forceinline__ int32_t rank_value(const WalkCtx& c, int32_t fc) {
 }
 
 // N independent row-only walks advanced in lockstep until each reaches a leaf
-// or a clock node (feat < 0, i.e. fc < 0).  Invalid walks only load their
-// start node.
+// or a clock node (feat < 0, i.e. fc < 0).  Walks enter LOADED (key / fc
+// describe node n).  A step whose child is a leaf (the parent's flag bits)
+// synthesizes it -- {leaf position, packed index = grid root + position,
+// kLeafFc} -- instead of loading it; lanes that do not advance reload the
+// root (always in the window) so the loop stays branch-free.
 template <bool kAllSmem, int N>
 __device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], const bool (&v)[N], Walk (&w)[N]) {
     bool g[N];
     bool any = false;
 #pragma unroll
     for (int h = 0; h < N; ++h) {
-        load_wnode<kAllSmem>(c, s[h], w[h]);
         g[h] = v[h] && w[h].fc >= 0;
         any |= g[h];
     }
@@ -227,9 +232,16 @@ __device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], c
         any = false;
 #pragma unroll
         for (int h = 0; h < N; ++h) {
-            const int32_t nn = wchild(w[h].fc) + (x[h] <= w[h].key ? 0 : 8);
-            w[h].n = g[h] ? nn : w[h].n;
-            load_wnode<kAllSmem>(c, s[h], w[h]);
+            const int right = x[h] <= w[h].key ? 0 : 1;
+            const int32_t nn = wchild(w[h].fc) + 8 * right;
+            const bool lf = (w[h].fc >> right) & 1;
+            Walk t{g[h] && !lf ? nn : 0, 0, 0};
+            load_wnode<kAllSmem>(c, s[h], t);
+            if (g[h]) {
+                w[h].n = nn;
+                w[h].key = lf ? s[h].groot + (nn >> 3) : t.key;
+                w[h].fc = lf ? kLeafFc : t.fc;
+            }
             g[h] = g[h] && w[h].fc >= 0;
             any |= g[h];
         }
@@ -254,7 +266,15 @@ __device__ __forceinline__ uint2 test_mk(const Walk& w) {
 
 __device__ __forceinline__ double leaf_value(const WalkCtx& c, const Walk& w) { return __ldg(&c.gnodes[w.key].v); }
 
-__device__ __forceinline__ Walk child_walk(const Walk& w, int side) { return Walk{wchild(w.fc) + 8 * side, 0, 0}; }
+// Child `side` of node w, loaded (or synthesized when the parent flags it a leaf).
+template <bool kAllSmem>
+__device__ __forceinline__ Walk child_walk(const WalkCtx& c, const TreeSrc& s, const Walk& w, int side) {
+    const int32_t nn = wchild(w.fc) + 8 * side;
+    if ((w.fc >> side) & 1) return Walk{nn, s.groot + (nn >> 3), kLeafFc};
+    Walk t{nn, 0, 0};
+    load_wnode<kAllSmem>(c, s, t);
+    return t;
+}
 
 // Resolve a tree whose root walk stopped at clock node `w` into its record:
 // one test between two leaves -> SM / MEM; a residue of depth <= 3 -> a
@@ -264,7 +284,7 @@ template <bool kAllSmem>
 __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const WalkCtx& c, const TreeSrc& s,
                                                    const Walk& w) {
     TreeRec r{0u, 0, 0, 0u};
-    Walk A = child_walk(w, 0), B = child_walk(w, 1);
+    Walk A = child_walk<kAllSmem>(c, s, w, 0), B = child_walk<kAllSmem>(c, s, w, 1);
     walk2<kAllSmem>(c, s, true, A, true, B);
     const bool ac = A.fc < 0 && wfeat(A.fc) != kFeatLeaf, bc = B.fc < 0 && wfeat(B.fc) != kFeatLeaf;
     if (!ac && !bc) {
@@ -285,12 +305,12 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
     const uint2 left = make_uint2(0u, 0u);
     Walk X[4] = {A, A, B, B};
     if (ac) {
-        X[0] = child_walk(A, 0);
-        X[1] = child_walk(A, 1);
+        X[0] = child_walk<kAllSmem>(c, s, A, 0);
+        X[1] = child_walk<kAllSmem>(c, s, A, 1);
     }
     if (bc) {
-        X[2] = child_walk(B, 0);
-        X[3] = child_walk(B, 1);
+        X[2] = child_walk<kAllSmem>(c, s, B, 0);
+        X[3] = child_walk<kAllSmem>(c, s, B, 1);
     }
     walk2<kAllSmem>(c, s, ac, X[0], ac, X[1]);
     walk2<kAllSmem>(c, s, bc, X[2], bc, X[3]);
@@ -314,8 +334,8 @@ __device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const Wa
             test[3 + k] = xc ? test_mk(X[k]) : left;
             Walk L = X[k], R = X[k];
             if (xc) {
-                L = child_walk(X[k], 0);
-                R = child_walk(X[k], 1);
+                L = child_walk<kAllSmem>(c, s, X[k], 0);
+                R = child_walk<kAllSmem>(c, s, X[k], 1);
             }
             walk2<kAllSmem>(c, s, xc, L, xc, R);
             if (wfeat(L.fc) != kFeatLeaf || wfeat(R.fc) != kFeatLeaf) depth = 0;
@@ -487,16 +507,18 @@ __device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int
         const int32_t nt = p.n_trees[ii.model];
         const int32_t* wroots = p.wroots[ii.model];
         const int32_t* roots = p.roots[ii.model];
+        const int32_t* wint = p.wint[ii.model];
         const int32_t pr = q + lane;
         int32_t w = 1 << 20;  // > any stage; 32 of them cannot overflow
-        int32_t r0 = 0, r1 = 0, r2 = 0, g0 = 0, g1 = 0;
+        int32_t r0 = 0, r1 = 0, g0 = 0, g1 = 0, wa = 0, wb = 0;
         if (pr < ii.p1) {
             r0 = __ldg(wroots + 2 * pr);
             r1 = __ldg(wroots + min(2 * pr + 1, nt));
-            r2 = __ldg(wroots + min(2 * pr + 2, nt));
             g0 = __ldg(roots + 2 * pr);
             g1 = 2 * pr + 1 < nt ? __ldg(roots + 2 * pr + 1) : 0;
-            w = min(r1 - r0, p.win_nodes) + min(r2 - r1, p.win_nodes);
+            wa = min(__ldg(wint + 2 * pr), p.win_nodes);
+            wb = 2 * pr + 1 < nt ? min(__ldg(wint + 2 * pr + 1), p.win_nodes) : 0;
+            w = wa + wb;
         }
         int32_t incl = w;
 #pragma unroll
@@ -510,24 +532,19 @@ __device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int
         q += n;
         const WNode* nodes = p.wnodes[ii.model];
         if (lane < n) {
-            const int32_t wa = min(r1 - r0, p.win_nodes), wb = min(r2 - r1, p.win_nodes);
             const uint32_t off = 8u * static_cast<uint32_t>(incl - w);
             const int k = 2 * lane;  // table index of tree 2 * pr
             table[k] = make_int4(r0, g0, wa, static_cast<int>(buf_saddr + off));
             if (2 * pr + 1 < nt) table[k + 1] = make_int4(r1, g1, wb, static_cast<int>(buf_saddr + off + 8u * wa));
-            if (!kAllSmem) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                bulk_g2s(buf_saddr + off, nodes + r0, 8u * static_cast<uint32_t>(wa), bar);
-                if (2 * pr + 1 < nt && wb > 0) bulk_g2s(buf_saddr + off + 8u * wa, nodes + r1, 8u * static_cast<uint32_t>(wb), bar);
-            }
+            // Each tree's window is its own bulk copy (windows are prefixes).
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            bulk_g2s(buf_saddr + off, nodes + r0, 8u * static_cast<uint32_t>(wa), bar);
+            if (2 * pr + 1 < nt && wb > 0) bulk_g2s(buf_saddr + off + 8u * wa, nodes + r1, 8u * static_cast<uint32_t>(wb), bar);
         }
         const uint32_t total = 8u * static_cast<uint32_t>(__shfl_sync(kFull, incl, n - 1));
-        const int32_t first = __shfl_sync(kFull, r0, 0);
         __syncwarp();  // the table entries are visible before lane 0's arrive releases them
         if (lane == 0) {
             *desc = st;  // published by the barrier's phase completion
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (kAllSmem) bulk_g2s(buf_saddr, nodes + first, total, bar);
             mbar_expect_tx(bar, total);
         }
         return;
@@ -671,6 +688,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
                 src[h].win = kAllSmem ? 0xffffffffu : static_cast<uint32_t>(e.z);
                 src[h].saddr = static_cast<uint32_t>(e.w);
                 w[h] = Walk{0, 0, 0};
+                load_wnode<kAllSmem>(c, src[h], w[h]);
             }
             walkn<kAllSmem, NW>(c, src, vv, w);
 #pragma unroll
@@ -1704,7 +1722,7 @@ WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 
     WalkGeom g{};
     g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
     g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
-    const int32_t max_tree = (p.max_tree_nodes + 1) & ~1;
+    const int32_t max_tree = (p.max_wint + 1) & ~1;  // the loadable prefixes are what is staged
     // 16 warps per CTA: 16 groups x 1 warp (512 apps per tile, every warp
     // walks every tree of a stage) or 8 groups x 2 warps (even / odd trees).
     g.n_subs = static_cast<int>(env_i64("GDVFS_WALK_SUBS", 1)) == 2 ? 2 : 1;
@@ -1831,7 +1849,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     }
     // 16-bit ranks and tree-local child indices bound what the walk handles.
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
-    const bool all_smem = ((p.max_tree_nodes + 1) & ~1) <= wg.win_nodes;
+    const bool all_smem = ((p.max_wint + 1) & ~1) <= wg.win_nodes;
     auto walk_kern = all_smem ? grid_walk_kernel<true> : grid_walk_kernel<false>;
     int walk_per_sm = occupancy(reinterpret_cast<const void*>(walk_kern), wg.warps * 32, wg.smem);
     if (walk_per_sm < 0) return cudaErrorInvalidConfiguration;
@@ -1874,6 +1892,8 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.wroots[1] = p.t_wroots;
         w.roots[0] = p.e_roots;
         w.roots[1] = p.t_roots;
+        w.wint[0] = p.e_wint;
+        w.wint[1] = p.t_wint;
         w.gnodes[0] = p.e_nodes;
         w.gnodes[1] = p.t_nodes;
         w.n_trees[0] = p.e_trees;

@@ -86,6 +86,11 @@ struct gd_model {
     int32_t* d_thr_off = nullptr;
     int32_t* d_wroots = nullptr;
     int64_t n_wnodes = 0;
+    // Per tree: walk nodes a walk can load -- the breadth-first prefix up to
+    // the last internal node (leaves are never loaded: parents flag them),
+    // rounded up to an even count.
+    int32_t* d_wint = nullptr;
+    int32_t max_wint = 0;
     int32_t max_thr_per_feature = 0;
     mutable gd::WNode* d_wnodes = nullptr;
     mutable int32_t grid_sm_col = -1, grid_mem_col = -1;

@@ -359,7 +359,11 @@ __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t 
                 const int32_t r = rank_of(thr + o, c, x.v);
                 w.key = (x.v == x.v && r < c) ? r : -1;  // exact match; NaN thresholds never pass
             }
-            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 19) | (static_cast<uint32_t>(child) * 8u));
+            // Leaf flags in the free low bits of the child offset: bit 0 the
+            // left child is a leaf, bit 1 the right one -- a walk stops at
+            // the parent and never loads a leaf node.
+            const uint32_t lf = (grid[x.aux].feat == kFeatLeaf ? 1u : 0u) | (grid[x.aux + 1].feat == kFeatLeaf ? 2u : 0u);
+            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 19) | (static_cast<uint32_t>(child) * 8u) | lf);
         }
         dst[__ldg(wroots + lo) + (i - root)] = w;
     }
