@@ -232,6 +232,23 @@ class Arm:
         self.bud_d.copy_(torch.from_numpy(self.budgets))
         torch.cuda.synchronize(dev)
 
+    def attach_comm(self, comm):
+        """The decision gather of N > 1 ranks (gd_comm, one NCCL gather to rank 0)."""
+        import torch
+
+        from paper_2004_08177_b200 import shard
+
+        self.comm = comm
+        self.counts = [hi - lo for lo, hi in (shard.shard_range(self.n_total, r, self.world) for r in range(self.world))]
+        self.recv_d = (torch.empty(self.n_total * shard.DECISION_BYTES, dtype=torch.uint8, device=self.dev)
+                       if comm is not None and self.rank == 0 else None)
+
+    def gather(self):
+        """Enqueue the gather on the context stream; rank 0 gets every app's decision (recv_d)."""
+        self.comm.gather_decisions(self.out_d.data_ptr(), self.counts,
+                                   self.recv_d.data_ptr() if self.recv_d is not None else 0, 0)
+        return self.recv_d
+
     def launch(self):
         import paper_2004_08177_b200 as gd
 
@@ -279,6 +296,14 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     ctx = gd.Context(local_rank)
+    comm = None
+    if world > 1:
+        # The decision gather runs through the library's own NCCL
+        # communicator (gd_comm): rank 0 makes the id, torch.distributed
+        # only carries it.
+        box = [gd.Comm.make_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        comm = gd.Comm(ctx, box[0], world, rank)
     # One explicit (non-default) stream for everything: torch's flush kernels,
     # the CUDA events and our launches.
     stream = torch.cuda.Stream(dev)
@@ -287,6 +312,7 @@ def run_ours(args, rank, world, local_rank):
 
     t_setup = time.perf_counter()
     arm = Arm(args.config, rank, world, dev, ctx, stream, args.apps, args.w_clk)
+    arm.attach_comm(comm)
     setup_s = time.perf_counter() - t_setup
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     sampler = None
@@ -322,7 +348,7 @@ def device_steps(arm, steps, warmup, world, stream, flush, gather=True):
         if ev is not None:
             ev[1].record(stream)
         if world > 1 and gather:
-            shard.gather_decisions(arm.out_d, arm.n_total, world)
+            arm.gather()
         if ev is not None:
             ev[2].record(stream)
 
@@ -400,7 +426,7 @@ def timed_main(args, arm, rank, world, dev, stream, ctx, flush, sampler):
             arm.cat_d.copy_(h_cat, non_blocking=True)
             arm.bud_d.copy_(h_bud, non_blocking=True)
             arm.launch()
-            full = shard.gather_decisions(arm.out_d, arm.n_total, world)
+            full = arm.gather()
             if rank == 0:
                 full_h.copy_(full, non_blocking=True)
             torch.cuda.synchronize(dev)
@@ -416,7 +442,7 @@ def timed_main(args, arm, rank, world, dev, stream, ctx, flush, sampler):
             e2e_times.append(time.perf_counter() - t0)
         h2d = int(arm.A * (arm.F + arm.K + 1) * 8)
         d2h = int(arm.n_total * shard.DECISION_BYTES) if rank == 0 else 0
-        api = "grid_select_device on each rank's shard (H2D from pinned host) + NCCL gather to rank 0 + D2H"
+        api = "grid_select_device on each rank's shard (H2D from pinned host) + gd_gather_decisions (NCCL gather to rank 0) + D2H"
         host_dec = full_h.numpy()[: arm.A * shard.DECISION_BYTES].view(gd.DECISION_DTYPE) if rank == 0 else None
     e2e_s, e2e_max = _max_over_ranks([float(np.mean(e2e_times)), float(np.max(e2e_times))], world, dev)
 

@@ -236,6 +236,43 @@ int gd_schedule_edf_frontier(const gd_job* jobs, int64_t n_jobs, const double* e
                              const gd_select_opts* opts, const double* exec_time, gd_exec_fn exec_fn,
                              void* exec_user, gd_decision* out, int64_t* order);
 
+/* Multi-GPU: query-row sharding ------------------------------
+ * Under full_deadline apps are independent (scheduler.cpp:203-205), so the
+ * grid path shards by contiguous app ranges (rank g of G owns apps
+ * [A*g/G, A*(g+1)/G)) with a replica of both ensembles per device; the only
+ * collective is one NCCL gather of the 24-byte decisions to the root.  NCCL
+ * is loaded at first use (libnccl.so.2; GDVFS_NCCL_LIB overrides); without
+ * it these calls return GD_ERR_UNSUPPORTED. */
+typedef struct gd_comm gd_comm;
+typedef struct gd_multi gd_multi;
+
+/* One process per GPU (torchrun): rank 0 creates a 128-byte id, every rank
+ * receives it out of band and joins with its context's device. */
+int gd_comm_unique_id(void* id128);
+int gd_comm_init_rank(gd_ctx* ctx, const void* id128, int32_t n_ranks, int32_t rank, gd_comm** out);
+int gd_comm_destroy(gd_comm* comm);
+/* The decision gather: rank r contributes counts[r] decisions (d_send, device
+ * memory); root receives them in rank order at d_recv (sum of counts).  Every
+ * rank calls it with the same counts; enqueued on the context stream. */
+int gd_gather_decisions(gd_comm* comm, const gd_decision* d_send, const int64_t* counts, gd_decision* d_recv,
+                        int32_t root);
+
+/* One process driving several GPUs: a context per device + ncclCommInitAll. */
+int gd_multi_create(const int32_t* devices, int32_t n_devices, gd_multi** out);
+int gd_multi_destroy(gd_multi* multi);
+int32_t gd_multi_size(const gd_multi* multi);
+int gd_multi_ctx(gd_multi* multi, int32_t index, gd_ctx** out);
+/* A copy of `src` (a model of any context, or host-only) on every device of
+ * the group: replicas[0 .. size-1], freed with gd_model_free. */
+int gd_multi_model_replicate(gd_multi* multi, const gd_model* src, gd_model** replicas);
+/* gd_grid_select (host buffers) row-sharded over the group: one host thread
+ * per device evaluates its app range, E/T tables (nullable) land directly in
+ * the caller's arrays, decisions are gathered to the first device by one
+ * NCCL gather and copied back once.  energy[i] / time[i] are the replicas on
+ * device i.  Results are identical to gd_grid_select on one device. */
+int gd_multi_grid_select(gd_multi* multi, gd_model* const* energy, gd_model* const* time, const gd_grid* grid,
+                         const gd_select_opts* opts, gd_decision* out, double* e_out, double* t_out);
+
 /* Measure this device's FP64 add throughput (adds/s) with independent
  * __dadd_rn chains: the peak of the path's binding roofline (in-order FP64
  * leaf sums), measured on the same box as the kernel it bounds. */

@@ -33,9 +33,17 @@
 
 namespace gpudvfs::gpu {
 
-/// The device the drop-in API runs on (one gd_ctx per host thread; device 0
-/// unless select_device() is called first on that thread).
+/// The device the drop-in API runs on (one gd_ctx per (host thread, device),
+/// kept for the thread's lifetime; device 0 unless select_device() is called
+/// first on that thread).  A predictor keeps the device(s) selected when it
+/// was made.
 void select_device(int device);
+
+/// Row-shard the predictors made after this call on this thread over several
+/// devices: one replica of each model per device, contiguous
+/// matched-app ranges per device, one NCCL gather of the decisions
+/// (gd_multi_grid_select).  Results are identical to one device.
+void select_devices(const std::vector<int>& devices);
 
 /// models::predict on the GPU (kernel K1): one value per row, energy clamped
 /// at 0, identical bits.  Throws std::invalid_argument naming the first

@@ -48,12 +48,19 @@ int main(int argc, char** argv) {
     const int iters = argc > 1 ? std::atoi(argv[1]) : 100;
     const int depth = argc > 2 ? std::atoi(argv[2]) : 10;
     const int n_jobs = argc > 3 ? std::atoi(argv[3]) : 100;
+    // catalog profiling stride: 2 = every other clock (each candidate its own
+    // nearest record -> general kernel); 25 = three records per app (clocks
+    // share records -> (app, record) virtual apps on the fast path)
+    const int stride = argc > 4 ? std::atoi(argv[4]) : 2;
+    // 1: the drop-in runs through a gd_multi device group (select_devices)
+    const bool multi = argc > 5 && std::atoi(argv[5]) != 0;
+    if (multi) gpu::select_devices({0});
     const std::uint64_t seed = 7;
     const std::string dir = std::filesystem::temp_directory_path() / "gd_facade_test";
     std::filesystem::create_directories(dir);
 
     synth::SyntheticGpu p100 = synth::builtin_p100_gpu();
-    Dataset catalog = p100.generate_dataset(synth::builtin_default_suite(), 2);
+    Dataset catalog = p100.generate_dataset(synth::builtin_default_suite(), stride);
     ingest::EncodeResult enc_e = ingest::encode(catalog, catalog, TargetKind::energy, 1.0, seed);
     ingest::EncodeResult enc_t = ingest::encode(catalog, catalog, TargetKind::time, 1.0, seed);
     models::GBTConfig cfg{iters, depth, 0.1, 3.0, seed};
@@ -84,6 +91,20 @@ int main(int argc, char** argv) {
     sched::WorkloadGenConfig gen;
     gen.seed = seed;
     Workload workload = sched::generate_workload(defaults, p100.device(), gen);
+    // Duplicate app_ids whose default profiles differ: the reference's
+    // predictor caches the FIRST PROCESSED job's correlation per app_id
+    // (scheduler.cpp:316-327), which the drop-in must reproduce.
+    {
+        std::vector<Job> jobs = workload.jobs;
+        const std::size_t n0 = jobs.size();
+        for (std::size_t i = 0; i + n0 / 2 < n0 && i < n0 / 4; ++i) {
+            Job d = jobs[i + n0 / 2];
+            d.app_id = jobs[i].app_id;
+            d.arrival_s = jobs[i].arrival_s + 0.25 * static_cast<double>(i % 3);
+            jobs.push_back(d);
+        }
+        workload = make_workload(std::move(jobs), p100.device());
+    }
     sched::ExecutionTimeSource exec = sched::make_truth_exec(queries, p100);
 
     sched::ClockPredictor ref_pred = sched::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog,

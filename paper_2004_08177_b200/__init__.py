@@ -33,7 +33,7 @@ from ._capi import GdError
 from .workload import Forest, GridInputs
 
 __all__ = [
-    "Context", "Model", "SchedulerOptions", "DECISION_DTYPE", "predict", "grid_select", "select",
+    "Context", "Model", "Comm", "Multi", "SchedulerOptions", "DECISION_DTYPE", "predict", "grid_select", "select",
     "schedule_d_dvfs", "DataError", "MissingArtifactError", "GdError", "Forest", "GridInputs",
 ]
 
@@ -136,9 +136,9 @@ class Context:
         return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
 
     def close(self) -> None:
-        if self._h:
+        if self._h and getattr(self, "_owned_by", None) is None:  # a Multi's contexts die with the group
             _capi.lib().gd_ctx_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         try:
@@ -408,3 +408,102 @@ def microbench_dadd(ctx: Optional[Context] = None) -> float:
     v = C.c_double()
     _raise(_capi.lib().gd_microbench_dadd(ctx.handle, C.byref(v)))
     return float(v.value)
+
+
+class Comm:
+    """One rank of a one-process-per-GPU group (gd_comm): the decision gather
+    of the row-sharded grid path over NCCL.  ``unique_id`` is made
+    on one rank (:meth:`make_id`) and shared out of band (e.g. a
+    torch.distributed broadcast)."""
+
+    def __init__(self, ctx: Context, unique_id: bytes, n_ranks: int, rank: int):
+        if len(unique_id) != 128:
+            raise ValueError("Comm: the NCCL unique id is 128 bytes")
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_comm_init_rank(ctx.handle, buf, n_ranks, rank, C.byref(h)))
+        self._h, self.ctx, self.n_ranks, self.rank = h, ctx, n_ranks, rank
+
+    @staticmethod
+    def make_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _raise(_capi.lib().gd_comm_unique_id(buf))
+        return bytes(buf)
+
+    def gather_decisions(self, d_send: int, counts, d_recv: int = 0, root: int = 0) -> None:
+        """Enqueue the gather: this rank's counts[rank] decisions at device
+        address d_send; root receives all of them in rank order at d_recv."""
+        cnt = np.ascontiguousarray(counts, np.int64)
+        if cnt.shape != (self.n_ranks,):
+            raise ValueError("Comm.gather_decisions: one count per rank")
+        _raise(_capi.lib().gd_gather_decisions(self._h, d_send or None, _ptr(cnt), d_recv or None, root))
+
+    def close(self) -> None:
+        if self._h:
+            _capi.lib().gd_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Multi:
+    """One process driving several GPUs (gd_multi): a context per device,
+    model replicas, and :meth:`grid_select` row-sharded over the devices with
+    one NCCL gather of the decisions."""
+
+    def __init__(self, devices: Sequence[int]):
+        dev = np.ascontiguousarray(devices, np.int32)
+        h = C.c_void_p()
+        _raise(_capi.lib().gd_multi_create(_ptr(dev), dev.shape[0], C.byref(h)))
+        self._h = h
+        self.devices = [int(d) for d in dev]
+        self.contexts = []
+        for i in range(len(self.devices)):
+            c = C.c_void_p()
+            _raise(_capi.lib().gd_multi_ctx(h, i, C.byref(c)))
+            ctx = Context.__new__(Context)
+            ctx._h, ctx.device = c, self.devices[i]
+            ctx._owned_by = self  # destroyed with the group, not by Context.close
+            self.contexts.append(ctx)
+
+    def replicate(self, model: "Model") -> list:
+        """A replica of `model` on every device of the group."""
+        n = len(self.devices)
+        arr = (C.c_void_p * n)()
+        _raise(_capi.lib().gd_multi_model_replicate(self._h, model.handle, arr))
+        return [Model(C.c_void_p(arr[i]), self.contexts[i]) for i in range(n)]
+
+    def grid_select(self, energy: Sequence["Model"], time: Sequence["Model"], grid: GridInputs, budgets,
+                    options: Optional[SchedulerOptions] = None, return_predictions: bool = False):
+        options = options or SchedulerOptions(budget="full")
+        budgets = _c(budgets, np.float64)
+        keep: list = []
+        g = _grid_struct(grid, budgets, keep)
+        a, c = grid.n_apps, grid.n_clocks
+        out = np.zeros(a, DECISION_DTYPE)
+        e = np.empty((a, c), np.float64) if return_predictions else None
+        t = np.empty((a, c), np.float64) if return_predictions else None
+        n = len(self.devices)
+        me = (C.c_void_p * n)(*[m.handle.value for m in energy])
+        mt = (C.c_void_p * n)(*[m.handle.value for m in time])
+        opts = options.opts()
+        _raise(_capi.lib().gd_multi_grid_select(self._h, me, mt, C.byref(g), C.byref(opts), _ptr(out), _ptr(e),
+                                                _ptr(t)))
+        return (out, e, t) if return_predictions else out
+
+    def close(self) -> None:
+        if self._h:
+            for ctx in self.contexts:
+                ctx._h = None
+            _capi.lib().gd_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

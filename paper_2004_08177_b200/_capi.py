@@ -116,6 +116,16 @@ SIGNATURES = {
     "gd_frontier": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P]),
     "gd_schedule_edf_frontier": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                                            C.POINTER(SelectOpts), _P, EXEC_FN, _P, _P, _P]),
+    "gd_comm_unique_id": (C.c_int, [_P]),
+    "gd_comm_init_rank": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "gd_comm_destroy": (C.c_int, [_P]),
+    "gd_gather_decisions": (C.c_int, [_P, _P, _P, _P, C.c_int32]),
+    "gd_multi_create": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "gd_multi_destroy": (C.c_int, [_P]),
+    "gd_multi_size": (C.c_int32, [_P]),
+    "gd_multi_ctx": (C.c_int, [_P, C.c_int32, C.POINTER(_P)]),
+    "gd_multi_model_replicate": (C.c_int, [_P, _P, _P]),
+    "gd_multi_grid_select": (C.c_int, [_P, _P, _P, C.POINTER(Grid), C.POINTER(SelectOpts), _P, _P, _P]),
 }
 
 

@@ -107,9 +107,14 @@ int activate(gd_ctx* ctx) {
     return GD_OK;
 }
 
-int check_model(const gd_model* m, const char* who) {
+int check_model(const gd_ctx* ctx, const gd_model* m, const char* who) {
     if (!m) return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": null model");
-    if (!m->ctx) return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": host-only model (no gd_ctx)");
+    if (m->device < 0) return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": host-only model (no gd_ctx)");
+    if (m->device != ctx->device) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, std::string(who) + ": model lives on device " +
+                                                      std::to_string(m->device) + ", context on device " +
+                                                      std::to_string(ctx->device));
+    }
     return GD_OK;
 }
 
@@ -166,7 +171,7 @@ int upload_model(gd_model* m) {
             wint.push_back(w < 2 ? 2 : w);
             if (wint.back() > m->max_wint) m->max_wint = wint.back();
         }
-        if (!m->ctx) return GD_OK;  // host-only model: validated, never uploaded
+        if (m->device < 0) return GD_OK;  // host-only model: validated, never uploaded
         if (!thr.empty()) {
             GD_CUDA(cudaMalloc(&m->d_thr, thr.size() * sizeof(double)), "cudaMalloc(thresholds)");
             GD_CUDA(cudaMemcpy(m->d_thr, thr.data(), thr.size() * sizeof(double), cudaMemcpyHostToDevice),
@@ -194,7 +199,7 @@ int upload_model(gd_model* m) {
                     "cudaMemcpy(roots)");
         }
     } else {
-        if (m->ctx && !m->coef.empty()) {
+        if (m->device >= 0 && !m->coef.empty()) {
             GD_CUDA(cudaMalloc(&m->d_coef, m->coef.size() * sizeof(double)), "cudaMalloc(coef)");
             GD_CUDA(cudaMemcpy(m->d_coef, m->coef.data(), m->coef.size() * sizeof(double), cudaMemcpyHostToDevice),
                     "cudaMemcpy(coef)");
@@ -517,7 +522,7 @@ int gd_model_upload_gbt(gd_ctx* ctx, const gd_forest_view* f, double base, doubl
     }
     auto* m = new gd_model;
     m->uid = next_model_uid();
-    m->ctx = ctx;
+    m->device = ctx ? ctx->device : -1;
     m->kind = GD_KIND_GBT;
     m->target = target;
     m->n_cols = n_cols;
@@ -556,7 +561,7 @@ int gd_model_upload_linear(gd_ctx* ctx, const double* coef, int32_t n_cols, doub
     if (kind != GD_KIND_OLS && kind != GD_KIND_LASSO) return set_error(GD_ERR_INVALID_ARGUMENT, "bad linear kind");
     auto* m = new gd_model;
     m->uid = next_model_uid();
-    m->ctx = ctx;
+    m->device = ctx ? ctx->device : -1;
     m->kind = kind;
     m->target = target;
     m->n_cols = n_cols;
@@ -580,7 +585,7 @@ int gd_model_load_file(gd_ctx* ctx, const char* path, gd_model** out) {
     if (rc) return rc;
     auto* m = new gd_model;
     m->uid = next_model_uid();
-    m->ctx = ctx;
+    m->device = ctx ? ctx->device : -1;
     rc = gdh::parse_model_file(path, *m);
     if (!rc) rc = upload_model(m);
     if (rc) {
@@ -591,6 +596,45 @@ int gd_model_load_file(gd_ctx* ctx, const char* path, gd_model** out) {
     *out = m;
     return GD_OK;
 }
+
+}  // extern "C"
+
+namespace gdh {
+
+int clone_model(gd_ctx* ctx, const gd_model* src, gd_model** out) {
+    if (!src || !out) return set_error(GD_ERR_INVALID_ARGUMENT, "clone_model: null argument");
+    *out = nullptr;
+    int rc = activate(ctx);
+    if (rc) return rc;
+    auto* m = new gd_model;
+    m->uid = next_model_uid();
+    m->device = ctx->device;
+    m->kind = src->kind;
+    m->target = src->target;
+    m->n_cols = src->n_cols;
+    m->base = src->base;
+    m->lr = src->lr;
+    m->offsets = src->offsets;
+    m->feature = src->feature;
+    m->left = src->left;
+    m->right = src->right;
+    m->threshold = src->threshold;
+    m->leaf = src->leaf;
+    m->coef = src->coef;
+    m->columns = src->columns;
+    rc = upload_model(m);
+    if (rc) {
+        release_model(m);
+        delete m;
+        return rc;
+    }
+    *out = m;
+    return GD_OK;
+}
+
+}  // namespace gdh
+
+extern "C" {
 
 int gd_model_info_get(const gd_model* m, gd_model_info* out) {
     if (!m || !out) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_info_get: null argument");
@@ -625,7 +669,7 @@ int gd_model_export(const gd_model* m, int64_t* tree_offsets, int32_t* feature, 
 
 int gd_model_free(gd_model* m) {
     if (!m) return GD_OK;
-    if (m->ctx) cudaSetDevice(m->ctx->device);
+    if (m->device >= 0) cudaSetDevice(m->device);
     release_model(m);
     delete m;
     return GD_OK;
@@ -635,7 +679,7 @@ int gd_predict_rows_device(gd_ctx* ctx, const gd_model* m, const double* d_rows,
                            double* d_out, int32_t* d_leaf) {
     int rc = activate(ctx);
     if (rc) return rc;
-    if ((rc = check_model(m, "predict"))) return rc;
+    if ((rc = check_model(ctx, m, "predict"))) return rc;
     if (n_rows < 0 || (n_rows > 0 && (!d_rows || !d_out))) return set_error(GD_ERR_INVALID_ARGUMENT, "predict: bad rows");
     return predict_rows_impl(ctx, m, d_rows, n_rows, n_cols, d_out, d_leaf);
 }
@@ -644,7 +688,7 @@ int gd_predict_rows(gd_ctx* ctx, const gd_model* m, const double* rows, int64_t 
                     int32_t* leaf_ids) {
     int rc = activate(ctx);
     if (rc) return rc;
-    if ((rc = check_model(m, "predict"))) return rc;
+    if ((rc = check_model(ctx, m, "predict"))) return rc;
     if (n_rows < 0 || (n_rows > 0 && (!rows || !out))) return set_error(GD_ERR_INVALID_ARGUMENT, "predict: bad rows");
     if (n_cols != m->n_cols) return predict_rows_impl(ctx, m, nullptr, 0, n_cols, nullptr, nullptr);
     if (n_rows == 0) return GD_OK;
@@ -675,7 +719,7 @@ int gd_grid_select_device(gd_ctx* ctx, const gd_model* me, const gd_model* mt, c
                           const gd_select_opts* o, gd_decision* d_out, double* d_e, double* d_t) {
     int rc = activate(ctx);
     if (rc) return rc;
-    if ((rc = check_model(me, "grid_select")) || (rc = check_model(mt, "grid_select"))) return rc;
+    if ((rc = check_model(ctx, me, "grid_select")) || (rc = check_model(ctx, mt, "grid_select"))) return rc;
     if ((rc = validate_grid(me, mt, g, o))) return rc;
     if (!d_out) return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null decisions");
     const double* rows_t = nullptr;
@@ -779,15 +823,19 @@ void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
 
 }  // namespace
 
-extern "C" {
+namespace gdh {
 
-int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
-                   gd_decision* out, double* e_out, double* t_out) {
+// gd_grid_select's body.  With keep_dev_out set, the decisions are left in
+// the context's persistent device buffer (*keep_dev_out, valid until the
+// next call on ctx) instead of being copied to `out`: the multi-device path
+// gathers them with NCCL (gd_multi.cpp).
+int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
+                     gd_decision* out, double* e_out, double* t_out, gd_decision** keep_dev_out) {
     int rc = activate(ctx);
     if (rc) return rc;
-    if ((rc = check_model(me, "grid_select")) || (rc = check_model(mt, "grid_select"))) return rc;
+    if ((rc = check_model(ctx, me, "grid_select")) || (rc = check_model(ctx, mt, "grid_select"))) return rc;
     if ((rc = validate_grid(me, mt, g, o))) return rc;
-    if (g->n_apps > 0 && (!out || !g->rows || !g->budgets || !g->sm_clock || !g->mem_clock ||
+    if (g->n_apps > 0 && ((!out && !keep_dev_out) || !g->rows || !g->budgets || !g->sm_clock || !g->mem_clock ||
                           (g->n_cat > 0 && (!g->cat_t || !g->cat_cols)))) {
         return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null input array");
     }
@@ -826,7 +874,7 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     const size_t i_t = s.add(t_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
     const size_t i_rt = s.add(g->rec_of_clock ? static_cast<size_t>(R) * g->n_cols * sizeof(double) : 0);
     const size_t in_end0 = s.pieces[i_bud].first + s.pieces[i_bud].second;
-    const bool graphable = graphs_enabled() && !ctx->timing && !g->rec_of_clock && !e_out && !t_out &&
+    const bool graphable = graphs_enabled() && !keep_dev_out && !ctx->timing && !g->rec_of_clock && !e_out && !t_out &&
                            in_end0 <= kStageLimit && static_cast<size_t>(A) * sizeof(gd_decision) <= kStageLimit;
     gd_graph_entry key;
     key.me = me->uid;
@@ -943,9 +991,13 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
                    static_cast<double*>(s.ptr(i_t)), rows_t, false);
     if (rc) return rc;
-    GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_out), static_cast<size_t>(A) * sizeof(gd_decision), cudaMemcpyDeviceToHost,
-                            ctx->stream),
-            "D2H decisions");
+    if (keep_dev_out) {
+        *keep_dev_out = static_cast<gd_decision*>(s.ptr(i_out));
+    } else {
+        GD_CUDA(cudaMemcpyAsync(out, s.ptr(i_out), static_cast<size_t>(A) * sizeof(gd_decision), cudaMemcpyDeviceToHost,
+                                ctx->stream),
+                "D2H decisions");
+    }
     if (e_out) {
         GD_CUDA(cudaMemcpyAsync(e_out, s.ptr(i_e), static_cast<size_t>(A) * C * sizeof(double), cudaMemcpyDeviceToHost,
                                 ctx->stream),
@@ -960,6 +1012,15 @@ int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
     if (graphable && ctx->stage) capture_graph(ctx, me, mt, dg, *o, key, s.base, in_end, static_cast<gd_decision*>(s.ptr(i_out)));
     return GD_OK;
+}
+
+}  // namespace gdh
+
+extern "C" {
+
+int gd_grid_select(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
+                   gd_decision* out, double* e_out, double* t_out) {
+    return gdh::grid_select_host(ctx, me, mt, g, o, out, e_out, t_out, nullptr);
 }
 
 int gd_select(gd_ctx* ctx, const double* energy, const double* time, int64_t n_apps, const int32_t* sm_clock,

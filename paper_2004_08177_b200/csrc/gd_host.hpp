@@ -55,7 +55,11 @@ struct gd_ctx {
 };
 
 struct gd_model {
-    gd_ctx* ctx = nullptr;
+    // Device the model lives on (-1: host-only, parsed / packed but never
+    // uploaded).  Models do not hold their creating gd_ctx: a context may be
+    // destroyed while its models live on, and a model serves any context of
+    // its device.
+    int device = -1;
     uint64_t uid = 0;  // process-unique (graph cache keys survive address reuse)
     int32_t kind = GD_KIND_GBT;
     int32_t target = GD_TARGET_ENERGY;
@@ -110,6 +114,16 @@ int pack_forest(const gd_forest_view& f, int32_t n_cols, std::vector<gd::PNode>&
 
 // "gpudvfs-model 1" parser (gd_model_io.cpp); fills the host fields of `m`.
 int parse_model_file(const char* path, gd_model& m);
+
+// gd_grid_select over host buffers; with keep_dev_out the decisions stay on
+// the device (*keep_dev_out, the context's persistent buffer) instead of
+// being copied to `out` (gd_capi.cpp).
+int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
+                     gd_decision* out, double* e_out, double* t_out, gd_decision** keep_dev_out);
+
+// A device copy of `src` (any model holding its host arrays) on ctx's device
+// (gd_capi.cpp; used by gd_multi_model_replicate).
+int clone_model(gd_ctx* ctx, const gd_model* src, gd_model** out);
 
 // Host selection for one job at a dynamic budget (gd_edf.cpp); the same
 // rules as the device epilogue.
