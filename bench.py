@@ -41,7 +41,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "(app×freq) energy+time predictions/sec and scheduling decisions/sec at 1/2/4/8 B200"
 UNIT = "predictions/s"
 L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
-CFG_INDEX = {"c2": 1, "c3": 2, "c4": 3, "c5": 4}
+CFG_INDEX = {"c2": 1, "c2t": 1, "c3": 2, "c4": 3, "c5": 4}
 DEADLINE_SEED = 77
 
 
@@ -86,6 +86,9 @@ def make_inputs(cfg, n_total, app_range, seed=1234, w_clk=None):
     slices of one n_total-app batch)."""
     from paper_2004_08177_b200 import workload as W
 
+    if cfg.get("trained"):
+        return W.make_trained_scenario("bench", n_total, cfg["catalog"], cfg["n_trees"], cfg["depth"], seed=seed,
+                                       app_range=app_range)
     kw = {} if w_clk is None else {"w_clk": w_clk}
     return W.make_scenario("bench", n_total, cfg["catalog"], cfg["n_trees"], cfg["depth"], seed=seed,
                            chunked=True, app_range=app_range, **kw)
@@ -135,7 +138,9 @@ def config_json(name, cfg, per_rank, n_total, world, n_clocks):
     return {"workload": f"BASELINE configs[{CFG_INDEX.get(name, -1)}] ({name}): {n_total} synthetic apps "
                         f"({'one batch row-sharded over' if name in STRONG else 'fixed per GPU on'} {world} GPU"
                         f"{'s' if world > 1 else ''}) x {n_clocks} {cfg['catalog']} clocks, {cfg['n_trees']}-tree "
-                        f"depth-{cfg['depth']} GBT energy + time, full_deadline text/energy",
+                        f"depth-{cfg['depth']} GBT energy + time"
+                        f"{' TRAINED on profiled records (GPU fit_gbt)' if cfg.get('trained') else ''}"
+                        f", full_deadline text/energy",
             "apps_per_gpu": per_rank, "apps_total": n_total, "clocks": n_clocks,
             "trees_per_model": cfg["n_trees"], "depth": cfg["depth"], "columns": 50,
             "parallelism": f"row-sharded dp{world}",
@@ -516,8 +521,10 @@ def extras(args, main_arm, dev, ctx, stream, flush):
     latency stream, beside the headline (N = 1)."""
     import torch
 
+    from paper_2004_08177_b200 import workload as W
+
     out = {}
-    for name in ("c3", "c2"):
+    for name in ("c3", "c2", "c2t"):
         if name == main_arm.name:
             continue
         try:
@@ -537,12 +544,27 @@ def extras(args, main_arm, dev, ctx, stream, flush):
                          "steps": steps, "warmup": 3, "kernels_ms": kern,
                          "acc_fp64_add_rate": dadd,
                          "decisions_per_s": arm.n_total / (step_ms * 1e-3)}
+            if name in ("c2", "c2t"):
+                # walk-record mix (CPU analysis of the first 48 apps): random
+                # synthetic trees vs trees trained on profiled records
+                out[name]["record_kinds"] = {
+                    m: W.record_kinds(f, arm.g.rows, arm.g.sm_col, arm.g.mem_col, max_apps=48)
+                    for m, f in (("energy", arm.sc.energy), ("time", arm.sc.time))}
             if name == "c2":
                 out["c5_latency"] = c5_latency(arm)
             del arm
             torch.cuda.empty_cache()
         except Exception as e:  # an extra must not cost the headline line
             out[name] = {"error": repr(e)}
+    try:
+        c1 = run_c1(argparse.Namespace(apps=100, steps=5), "ours")
+        out["c1"] = {k: c1[k] for k in ("config", "value", "unit", "ms_per_step", "decisions_per_s", "cpu_baseline",
+                                        "decisions_identical_to_reference")}
+        c1k = run_c1(argparse.Namespace(apps=1000, steps=3), "ours")
+        out["c1_1000_jobs"] = {k: c1k[k] for k in ("value", "ms_per_step", "decisions_per_s", "cpu_baseline",
+                                                   "decisions_identical_to_reference")}
+    except Exception as e:  # noqa: BLE001
+        out["c1"] = {"error": repr(e)}
     return out
 
 
@@ -573,8 +595,28 @@ def c5_latency(arm, batch=64, iters=300, warmup=30):
         if k >= warmup:
             lat.append(time.perf_counter() - t0)
     lat_us = np.array(lat) * 1e6
+    # CPU baseline of the same stream: the reference's predict + select per
+    # batch (oracle/_ref) on all host threads, 40 batches.
+    cpu = None
+    try:
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib as O
+
+        if O.ref_available():
+            threads = os.cpu_count() or 1
+            cl = []
+            for k in range(40):
+                gw, bw = wins[k % len(wins)]
+                secs, _ = O.ref_bench_grid(arm.sc.energy, arm.sc.time, gw, bw, batch, threads)
+                cl.append(secs * 1e6)
+            cl = np.array(cl)
+            cpu = {"kind": "reference", "cores": threads, "batches": 40, "p50_us": float(np.percentile(cl, 50)),
+                   "p99_us": float(np.percentile(cl, 99))}
+    except Exception as e:  # noqa: BLE001
+        cpu = {"error": repr(e)}
     return {"workload": "BASELINE configs[4] (c5): 64-job batches x 267 clocks, 500-tree depth-8 E + T, one "
                         "gd_grid_select per batch (host buffers)",
+            "cpu_reference": cpu,
             "p50_us": float(np.percentile(lat_us, 50)), "p99_us": float(np.percentile(lat_us, 99)),
             "mean_us": float(lat_us.mean()), "batches": iters,
             "decisions_per_s_at_p50": batch / (np.percentile(lat_us, 50) * 1e-6),
@@ -706,8 +748,60 @@ def _free_port():
         return s.getsockname()[1]
 
 
+FACADE = ROOT / "integration" / "_build" / "facade_test"
+
+
+def run_c1(args, impl):
+    """BASELINE configs[0], the paper-scale production path: the P100 catalog
+    (12 suite apps x 62 clocks, profiled at every other clock), fit_gbt 100 x
+    depth 10 energy + time, k-means clusters, then a cold make_model_predictor
+    + schedule_d_dvfs(full_deadline) over the job batch -- through the C++
+    drop-in (gpu_api.hpp) and through the reference's own functions, in one
+    process on the same inputs (integration/facade_test --bench).  Decisions
+    must be identical.  Host-side work (correlation, encoding, EDF) dominates
+    at this size; the GPU evaluates the 62 x 100-tree candidates."""
+    jobs = args.apps or 100
+    reps = max(1, args.steps)
+    if not FACADE.exists():
+        return {"impl": impl, "unavailable": "integration/_build/facade_test not built (needs the reference headers)"}
+    r = subprocess.run([str(FACADE), "--bench", str(reps), "100", "10", str(jobs)], capture_output=True, text=True,
+                       timeout=1800)
+    if r.returncode != 0:
+        raise RuntimeError(f"facade bench failed: {r.stdout[-500:]} {r.stderr[-500:]}")
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    preds = d["jobs"] * d["clocks"]
+    ms = d["reference_ms_median"] if impl == "reference" else d["dropin_ms_median"]
+    value = preds / (ms * 1e-3)
+    cfg = {"workload": f"BASELINE configs[0] (c1): paper-scale production path, P100 catalog "
+                       f"({d['catalog_records']} profiled records, {d['clocks']} clocks), fit_gbt {d['trees']} trees "
+                       f"depth {d['depth']} E + T, {d['jobs']}-job batch, cold predictor + schedule_d_dvfs "
+                       f"(full_deadline)", "jobs": d["jobs"], "clocks": d["clocks"], "parallelism": "dp1",
+           "api": "C++ drop-in gpu::make_model_predictor + gpu::schedule_d_dvfs" if impl != "reference" else
+                  "reference sched::make_model_predictor + sched::schedule_d_dvfs"}
+    res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": reps, "warmup": 1,
+           "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (the reference's own synthetic P100 GPU and suite; queries seeded)", "config": cfg,
+           "decisions_per_s": d["jobs"] / (ms * 1e-3),
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                   "note": "the C++ API call itself is the end-to-end path (host tables in, decisions out)"},
+           "decisions_identical_to_reference": d["decisions_identical"], "scheduled": d["scheduled"],
+           "facade": d}
+    if impl == "reference":
+        res["impl"] = "reference"
+        res["cpu_baseline"] = {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                               "sample": f"the whole {d['jobs']}-job batch"}
+        res["e2e"]["h2d_bytes_per_step"] = res["e2e"]["d2h_bytes_per_step"] = 0
+    else:
+        res["cpu_baseline"] = {"value": preds / (d["reference_ms_median"] * 1e-3), "unit": UNIT, "cores": 1,
+                               "kind": "reference", "sample": f"the whole {d['jobs']}-job batch, same process"}
+    return res
+
+
 def main():
     args = parse_args()
+    if args.config == "c1":
+        print(json.dumps(run_c1(args, args.impl)), flush=True)
+        return
     if args.gpus > 1 and "RANK" not in os.environ:
         # One process per GPU: re-execute under torch.distributed.run.
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",

@@ -236,6 +236,27 @@ int gd_schedule_edf_frontier(const gd_job* jobs, int64_t n_jobs, const double* e
                              const gd_select_opts* opts, const double* exec_time, gd_exec_fn exec_fn,
                              void* exec_user, gd_decision* out, int64_t* order);
 
+/* Training: fit_gbt on the GPU ------------------------------
+ * GBTConfig (models.hpp:18-24). */
+typedef struct gd_gbt_config {
+    int32_t iterations;
+    int32_t depth;
+    double learning_rate;
+    double l2_leaf_reg;
+    uint64_t seed;
+} gd_gbt_config;
+
+/* models::fit_gbt (models.cpp:381-393; GbtCore, models.cpp:161-368): the
+ * level-wise exact-greedy booster over presorted columns, with the split
+ * search, routing and residual updates on the device.  rows is the
+ * EncodedMatrix (n_rows x n_cols, row-major), targets its targets.  The
+ * returned model's trees are node for node those of fit_gbt (node order,
+ * features, thresholds, leaf values -- gd_model_export reads them) and it is
+ * uploaded on ctx, ready for prediction.  Errors: the reference's
+ * validate_config / require_rows messages (GD_ERR_INVALID_ARGUMENT). */
+int gd_fit_gbt(gd_ctx* ctx, const double* rows, int64_t n_rows, int32_t n_cols, const double* targets,
+               const gd_gbt_config* config, int32_t target, gd_model** out);
+
 /* Multi-GPU: query-row sharding ------------------------------
  * Under full_deadline apps are independent (scheduler.cpp:203-205), so the
  * grid path shards by contiguous app ranges (rank g of G owns apps

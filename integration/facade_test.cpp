@@ -7,6 +7,7 @@
 // decisions (job order, clock, predicted E/T bits, status, note) for every
 // SchedulerOptions combination; then models::predict vs gpu::predict and the
 // column-mismatch exception message.  Exit 0 = identical.
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -45,6 +46,15 @@ bool same(const sched::ScheduleDecision& a, const sched::ScheduleDecision& b) {
 }  // namespace
 
 int main(int argc, char** argv) {
+    // --bench [reps]: time the paper-scale production path (cold predictor +
+    // schedule_d_dvfs, full_deadline) through the reference and through the
+    // drop-in, `reps` times each, and print one JSON line (bench.py --config c1).
+    int bench_reps = 0;
+    if (argc > 1 && std::string(argv[1]) == "--bench") {
+        bench_reps = argc > 2 ? std::atoi(argv[2]) : 5;
+        argv += 2;
+        argc -= 2;
+    }
     const int iters = argc > 1 ? std::atoi(argv[1]) : 100;
     const int depth = argc > 2 ? std::atoi(argv[2]) : 10;
     const int n_jobs = argc > 3 ? std::atoi(argv[3]) : 100;
@@ -106,6 +116,44 @@ int main(int argc, char** argv) {
         workload = make_workload(std::move(jobs), p100.device());
     }
     sched::ExecutionTimeSource exec = sched::make_truth_exec(queries, p100);
+
+    if (bench_reps > 0) {
+        sched::SchedulerOptions o;
+        o.budget = sched::DeadlineBudget::full_deadline;
+        std::vector<double> ref_ms, gpu_ms;
+        bool identical = true;
+        int scheduled = 0;
+        for (int r = 0; r < bench_reps + 1; ++r) {  // the first repetition warms up
+            auto t0 = std::chrono::steady_clock::now();
+            sched::ClockPredictor rp =
+                sched::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog, clusters);
+            auto want = sched::schedule_d_dvfs(workload, rp, exec, o);
+            auto t1 = std::chrono::steady_clock::now();
+            sched::ClockPredictor gp =
+                gpu::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog, clusters);
+            auto got = gpu::schedule_d_dvfs(workload, gp, exec, o);
+            auto t2 = std::chrono::steady_clock::now();
+            identical = identical && want.size() == got.size();
+            scheduled = 0;
+            for (std::size_t k = 0; k < want.size() && k < got.size(); ++k) {
+                identical = identical && same(want[k], got[k]);
+                scheduled += got[k].status == sched::DecisionStatus::scheduled;
+            }
+            if (r == 0) continue;
+            ref_ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+            gpu_ms.push_back(std::chrono::duration<double, std::milli>(t2 - t1).count());
+        }
+        std::sort(ref_ms.begin(), ref_ms.end());
+        std::sort(gpu_ms.begin(), gpu_ms.end());
+        std::printf("{\"jobs\": %zu, \"clocks\": %zu, \"catalog_records\": %zu, \"trees\": %d, \"depth\": %d, "
+                    "\"reps\": %d, \"reference_ms_median\": %.4f, \"dropin_ms_median\": %.4f, "
+                    "\"reference_ms_min\": %.4f, \"dropin_ms_min\": %.4f, \"scheduled\": %d, "
+                    "\"decisions_identical\": %s}\n",
+                    workload.jobs.size(), clock_catalog(catalog.device).size(), catalog.records.size(), iters, depth,
+                    bench_reps, ref_ms[ref_ms.size() / 2], gpu_ms[gpu_ms.size() / 2], ref_ms.front(), gpu_ms.front(),
+                    scheduled, identical ? "true" : "false");
+        return identical ? 0 : 1;
+    }
 
     sched::ClockPredictor ref_pred = sched::make_model_predictor(me, enc_e.metadata, mt, enc_t.metadata, catalog,
                                                                  clusters);

@@ -836,6 +836,7 @@ std::vector<sched::ScheduleDecision> schedule_d_dvfs(const Workload& workload, c
         }
         // Leave the predictor in the state the reference's would be in.
         for (const auto& [app, j] : decider) {
+            if (st.cache.count(app) || st.failed.count(app)) continue;  // decided by an earlier query
             TablePtr t = st.table_for_match(match[static_cast<std::size_t>(j)]);
             if (t) st.cache[app] = t;
             else st.failed.insert(app);

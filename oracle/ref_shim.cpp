@@ -429,6 +429,73 @@ int ref_c1_scenario(const char* out_dir, uint64_t seed, int stride, int iters, i
     }
 }
 
+// The encoded training matrix of the paper-scale C1 catalog (P100 suite at
+// `stride`, ingest::encode for `target`): rows == NULL returns the shape only.
+int ref_c1_train(uint64_t seed, int stride, int target, double* rows, double* targets, int64_t* n_rows,
+                 int32_t* n_cols) {
+    try {
+        synth::SyntheticGpu p100 = synth::builtin_p100_gpu();
+        Dataset catalog = p100.generate_dataset(synth::builtin_default_suite(), stride);
+        ingest::EncodeResult enc = ingest::encode(catalog, catalog, target == 0 ? TargetKind::energy : TargetKind::time,
+                                                  1.0, seed);
+        *n_rows = static_cast<int64_t>(enc.train.rows.size());
+        *n_cols = static_cast<int32_t>(enc.train.columns.size());
+        if (rows) {
+            for (std::size_t r = 0; r < enc.train.rows.size(); ++r) {
+                std::memcpy(rows + r * enc.train.columns.size(), enc.train.rows[r].data(),
+                            enc.train.columns.size() * sizeof(double));
+                targets[r] = enc.train.targets[r];
+            }
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// models::fit_gbt on a given matrix; the trees stay in fit_gbt's node order
+// (NOT reloaded).  ref_fit_gbt fits and keeps the model; ref_fit_gbt_export
+// copies it out (arrays sized by the n_trees / n_nodes ref_fit_gbt returned).
+thread_local models::FittedModel g_fit;
+int ref_fit_gbt(const double* rows, int64_t n_rows, int n_cols, const double* targets, int iterations, int depth,
+                double lr, double l2, uint64_t seed, int target, int32_t* n_trees, int64_t* n_nodes, double* base) {
+    try {
+        ingest::EncodedMatrix m = matrix_of(rows, n_rows, n_cols, column_names(n_cols));
+        m.targets.assign(targets, targets + n_rows);
+        m.target = target == 0 ? TargetKind::energy : TargetKind::time;
+        models::GBTConfig cfg{iterations, depth, lr, l2, seed};
+        g_fit = models::fit_gbt(m, cfg);
+        *n_trees = static_cast<int32_t>(g_fit.gbt.trees.size());
+        int64_t nn = 0;
+        for (const auto& t : g_fit.gbt.trees) nn += static_cast<int64_t>(t.nodes.size());
+        *n_nodes = nn;
+        *base = g_fit.gbt.base_prediction;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+int ref_fit_gbt_export(int64_t* offsets, int32_t* feature, double* threshold, int32_t* left, int32_t* right,
+                       double* leaf_value) {
+    int64_t k = 0;
+    offsets[0] = 0;
+    for (std::size_t t = 0; t < g_fit.gbt.trees.size(); ++t) {
+        for (const auto& n : g_fit.gbt.trees[t].nodes) {
+            feature[k] = n.feature;
+            threshold[k] = n.threshold;
+            left[k] = n.left;
+            right[k] = n.right;
+            leaf_value[k] = n.leaf_value;
+            ++k;
+        }
+        offsets[t + 1] = k;
+    }
+    return 0;
+}
+
 // Acceptance #1 material: truth E/T over the P100 catalog for
 // the 12 suite apps with noise offset `seed_offset`, and oracle_per_job's
 // decision for each app at the given relative deadlines (scheduler.cpp:257-281).

@@ -8,6 +8,7 @@ reference (proj/)                      here
 =====================================  ==========================================
 models::predict (models.cpp:395)       :func:`predict` / :meth:`Model.predict`
 models::load_model_file (:710)         :meth:`Model.load_file`
+models::fit_gbt (models.cpp:381)       :func:`fit_gbt` (booster on the GPU)
 make_model_predictor + build           :func:`grid_select` (rows generated on
   (scheduler.cpp:329-394)                the fly, E/T fused with selection)
 select_text / select_literal /         :func:`select` (K3 over given E/T),
@@ -33,7 +34,7 @@ from ._capi import GdError
 from .workload import Forest, GridInputs
 
 __all__ = [
-    "Context", "Model", "Comm", "Multi", "SchedulerOptions", "DECISION_DTYPE", "predict", "grid_select", "select",
+    "Context", "Model", "Comm", "Multi", "SchedulerOptions", "fit_gbt", "DECISION_DTYPE", "predict", "grid_select", "select",
     "schedule_d_dvfs", "DataError", "MissingArtifactError", "GdError", "Forest", "GridInputs",
 ]
 
@@ -254,6 +255,25 @@ def predict(model: Model, rows, leaf_ids: bool = False, columns: Optional[Sequen
     _raise(_capi.lib().gd_predict_rows(model.ctx.handle, model.handle, _ptr(rows), rows.shape[0], rows.shape[1],
                                        _ptr(out), _ptr(ids)))
     return (out, ids) if leaf_ids else out
+
+
+def fit_gbt(rows, targets, iterations: int = 400, depth: int = 4, learning_rate: float = 0.1,
+            l2_leaf_reg: float = 3.0, seed: int = 0, target: int = 0, ctx: Optional[Context] = None) -> Model:
+    """models::fit_gbt (models.cpp:381-393) on the GPU: the same trees, node
+    for node (GBTConfig defaults of models.hpp:18-24).  Returns a device-
+    resident Model; ``Model.export()`` gives the trees in fit_gbt's order."""
+    ctx = ctx or default_context()
+    rows = _c(rows, np.float64)
+    targets = _c(targets, np.float64)
+    if rows.ndim != 2:
+        raise ValueError("fit_gbt: rows must be a 2-D array")
+    if targets.shape != (rows.shape[0],):
+        raise ValueError("fit_gbt: row/target count mismatch")
+    cfg = _capi.GbtConfig(iterations, depth, learning_rate, l2_leaf_reg, seed)
+    h = C.c_void_p()
+    _raise(_capi.lib().gd_fit_gbt(ctx.handle, _ptr(rows) if rows.size else None, rows.shape[0], rows.shape[1],
+                                  _ptr(targets) if targets.size else None, C.byref(cfg), target, C.byref(h)))
+    return Model(h, ctx)
 
 
 def _check_columns(model_cols, row_cols):

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib" / "libgdvfs.so"
-SOURCES = ["gd_grid.cu", "gd_kernels.cu", "gd_capi.cpp", "gd_pack.cpp", "gd_model_io.cpp", "gd_edf.cpp", "gd_multi.cpp"]
+SOURCES = ["gd_grid.cu", "gd_kernels.cu", "gd_capi.cpp", "gd_pack.cpp", "gd_model_io.cpp", "gd_edf.cpp", "gd_multi.cpp", "gd_train.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -72,6 +72,11 @@ class SelectOpts(C.Structure):
     _fields_ = [("mode", C.c_int32), ("objective", C.c_int32), ("best_effort", C.c_int32), ("pad", C.c_int32)]
 
 
+class GbtConfig(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("depth", C.c_int32), ("learning_rate", C.c_double),
+                ("l2_leaf_reg", C.c_double), ("seed", C.c_uint64)]
+
+
 class Job(C.Structure):
     _fields_ = [
         ("arrival_s", C.c_double),
@@ -116,6 +121,7 @@ SIGNATURES = {
     "gd_frontier": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P, _P]),
     "gd_schedule_edf_frontier": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_int32, C.c_int32,
                                            C.POINTER(SelectOpts), _P, EXEC_FN, _P, _P, _P]),
+    "gd_fit_gbt": (C.c_int, [_P, _P, C.c_int64, C.c_int32, _P, C.POINTER(GbtConfig), C.c_int32, C.POINTER(_P)]),
     "gd_comm_unique_id": (C.c_int, [_P]),
     "gd_comm_init_rank": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(_P)]),
     "gd_comm_destroy": (C.c_int, [_P]),

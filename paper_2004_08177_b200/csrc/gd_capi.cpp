@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -635,6 +636,42 @@ int clone_model(gd_ctx* ctx, const gd_model* src, gd_model** out) {
 }  // namespace gdh
 
 extern "C" {
+
+int gd_fit_gbt(gd_ctx* ctx, const double* rows, int64_t n_rows, int32_t n_cols, const double* targets,
+               const gd_gbt_config* cfg, int32_t target, gd_model** out) {
+    if (!out || !cfg) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_fit_gbt: null argument");
+    *out = nullptr;
+    int rc = activate(ctx);
+    if (rc) return rc;
+    // models.cpp:37-42 (require_rows) and :46-53 (validate_config), same messages.
+    if (n_rows <= 0 || !rows) return set_error(GD_ERR_INVALID_ARGUMENT, "fit_gbt: empty training matrix");
+    if (!targets) return set_error(GD_ERR_INVALID_ARGUMENT, "fit_gbt: row/target count mismatch");
+    if (cfg->iterations < 0) return set_error(GD_ERR_INVALID_ARGUMENT, "gbt config: iterations must be >= 0");
+    if (cfg->depth < 1) return set_error(GD_ERR_INVALID_ARGUMENT, "gbt config: depth must be >= 1");
+    if (!(cfg->learning_rate > 0.0) || cfg->learning_rate > 1.0) {
+        return set_error(GD_ERR_INVALID_ARGUMENT, "gbt config: learning_rate must lie in (0, 1]");
+    }
+    if (cfg->l2_leaf_reg < 0.0) return set_error(GD_ERR_INVALID_ARGUMENT, "gbt config: l2_leaf_reg must be >= 0");
+    if (n_cols < 0 || n_rows > INT32_MAX) return set_error(GD_ERR_INVALID_ARGUMENT, "fit_gbt: bad shape");
+    if (target != GD_TARGET_ENERGY && target != GD_TARGET_TIME) return set_error(GD_ERR_INVALID_ARGUMENT, "bad target");
+    auto* m = new gd_model;
+    m->uid = next_model_uid();
+    m->device = ctx->device;
+    m->kind = GD_KIND_GBT;
+    m->target = target;
+    m->n_cols = n_cols;
+    m->lr = cfg->learning_rate;
+    rc = gdh::fit_gbt_device(ctx, rows, n_rows, n_cols, targets, *cfg, m->offsets, m->feature, m->threshold, m->left,
+                             m->right, m->leaf, m->base);
+    if (!rc) rc = upload_model(m);
+    if (rc) {
+        release_model(m);
+        delete m;
+        return rc;
+    }
+    *out = m;
+    return GD_OK;
+}
 
 int gd_model_info_get(const gd_model* m, gd_model_info* out) {
     if (!m || !out) return set_error(GD_ERR_INVALID_ARGUMENT, "gd_model_info_get: null argument");

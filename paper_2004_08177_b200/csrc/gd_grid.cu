@@ -44,9 +44,14 @@
 #include <cstdlib>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <vector>
 
 #include "gd_common.cuh"
+
+#ifndef GD_RES_LEVELS
+#define GD_RES_LEVELS 4  // test levels a residue table holds (deeper: FULL)
+#endif
 
 namespace gd {
 #ifdef GD_WALK_TRACE
@@ -67,7 +72,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 // The walk -> accumulate hand-off.
 // ---------------------------------------------------------------------------
-enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4 };
+enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4, kRecTable4 = 5 };
 
 // One (app, tree) record.  info = kind | t16 << 16 (SM / MEM keys); leaves
 // are referenced by packed (grid) index and their values fetched by the
@@ -84,8 +89,10 @@ static_assert(sizeof(TreeRec) == 16, "TreeRec is 16 bytes");
 
 // A residue table: the clock-only residue of one (app, tree) as a balanced
 // tree of depth D (2 or 3).  Test k is node k (children 2k+1, 2k+2); a clock
-// goes right iff (ck & mask) > key (always-left = {0, 0}); leaf l is node
-// 2^D - 1 + l.
+// goes right iff (ck & mask) > key (always-left = {0, 0}).  Leaves are stored
+// in depth-3 slots whatever D is: the leaf a depth-D walk ends on (node
+// 2^D - 1 + l) is leaf[l << (3 - D)].  A leaf found at level k < D sits under
+// always-left tests, so it is read through its leftmost slot only.
 struct __align__(16) RTRec {
     uint2 test[7];
     uint32_t depth;
@@ -93,6 +100,15 @@ struct __align__(16) RTRec {
     double leaf[8];
 };
 static_assert(sizeof(RTRec) == 128, "RTRec is 128 bytes");
+
+// A depth-4 residue (two consecutive pool slots, record kind kRecTable4):
+// tests 0..14 in heap order, leaf l (node 15 + l) at leaf[l].
+struct __align__(16) RTRec4 {
+    uint2 test[15];
+    uint32_t pad[2];
+    double leaf[16];
+};
+static_assert(sizeof(RTRec4) == 256, "RTRec4 is two pool slots");
 
 
 // Records of tree t for batch-local app la: pairs of trees are interleaved
@@ -264,7 +280,6 @@ __device__ __forceinline__ uint2 test_mk(const Walk& w) {
     return wfeat(w.fc) == kFeatMem ? make_uint2(0xffffu, t) : make_uint2(0xffffffffu, (t << 16) | 0xffffu);
 }
 
-__device__ __forceinline__ double leaf_value(const WalkCtx& c, const Walk& w) { return __ldg(&c.gnodes[w.key].v); }
 
 // Child `side` of node w, loaded (or synthesized when the parent flags it a leaf).
 template <bool kAllSmem>
@@ -276,95 +291,151 @@ __device__ __forceinline__ Walk child_walk(const WalkCtx& c, const TreeSrc& s, c
     return t;
 }
 
-// Resolve a tree whose root walk stopped at clock node `w` into its record:
-// one test between two leaves -> SM / MEM; a residue of depth <= 3 -> a
-// residue table (balanced; a leaf above the last level is replicated under
-// always-left tests); deeper -> FULL.
-template <bool kAllSmem>
-__device__ __forceinline__ TreeRec resolve_residue(const WalkParams& p, const WalkCtx& c, const TreeSrc& s,
-                                                   const Walk& w) {
-    TreeRec r{0u, 0, 0, 0u};
-    Walk A = child_walk<kAllSmem>(c, s, w, 0), B = child_walk<kAllSmem>(c, s, w, 1);
-    walk2<kAllSmem>(c, s, true, A, true, B);
-    const bool ac = A.fc < 0 && wfeat(A.fc) != kFeatLeaf, bc = B.fc < 0 && wfeat(B.fc) != kFeatLeaf;
-    if (!ac && !bc) {
-        r.info = (wfeat(w.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w.key) << 16);
-        r.ref = A.key;
-        r.ref2 = B.key;
-        return r;
-    }
-    r.info = kRecFull;
-    r.ref = s.groot + (w.n >> 3);
-    // Warp-aggregated pool allocation among the lanes that got here together,
-    // issued now and consumed at the end: its round trip overlaps the
-    // grandchild walks and the leaf loads.
-    const unsigned am = __activemask();
-    const int lane = threadIdx.x & 31, leader = __ffs(am) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(p.pool_count, static_cast<uint32_t>(__popc(am)));
-    const uint2 left = make_uint2(0u, 0u);
-    Walk X[4] = {A, A, B, B};
-    if (ac) {
-        X[0] = child_walk<kAllSmem>(c, s, A, 0);
-        X[1] = child_walk<kAllSmem>(c, s, A, 1);
-    }
-    if (bc) {
-        X[2] = child_walk<kAllSmem>(c, s, B, 0);
-        X[3] = child_walk<kAllSmem>(c, s, B, 1);
-    }
-    walk2<kAllSmem>(c, s, ac, X[0], ac, X[1]);
-    walk2<kAllSmem>(c, s, bc, X[2], bc, X[3]);
-    uint2 test[7];
-    test[0] = test_mk(w);
-    test[1] = ac ? test_mk(A) : left;
-    test[2] = bc ? test_mk(B) : left;
-    bool deeper = false;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) deeper |= wfeat(X[k].fc) != kFeatLeaf;
-    double leaf[8];
-    int depth = 2;  // 0: deeper than 3 (FULL)
-    if (!deeper) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) leaf[k] = leaf_value(c, X[k]);
-    } else {
-        depth = 3;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const bool xc = wfeat(X[k].fc) != kFeatLeaf;
-            test[3 + k] = xc ? test_mk(X[k]) : left;
-            Walk L = X[k], R = X[k];
-            if (xc) {
-                L = child_walk<kAllSmem>(c, s, X[k], 0);
-                R = child_walk<kAllSmem>(c, s, X[k], 1);
-            }
-            walk2<kAllSmem>(c, s, xc, L, xc, R);
-            if (wfeat(L.fc) != kFeatLeaf || wfeat(R.fc) != kFeatLeaf) depth = 0;
-            if (depth) {
-                leaf[2 * k] = leaf_value(c, L);
-                leaf[2 * k + 1] = leaf_value(c, R);
-            }
-        }
-    }
-    const uint32_t idx = __shfl_sync(am, base, leader) + __popc(am & ((1u << lane) - 1u));
-    if (depth == 0 || idx >= p.pool_cap) return r;  // FULL (a slot left unused, as a deeper residue)
-    RTRec* q = p.pool + idx;
-    const int nt = depth == 2 ? 3 : 7, nl = depth == 2 ? 4 : 8;
-#pragma unroll
-    for (int k = 0; k < 7; ++k)
-        if (k < nt) q->test[k] = test[k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (k < nl) q->leaf[k] = leaf[k];
-    q->depth = depth;
-    r.info = kRecTable;
-    r.ref = static_cast<int32_t>(idx);
-    return r;
-}
-
 // Records are written once and read once by the accumulate kernel: stream
 // them past L2 (evict-first) so the models' nodes stay L2-resident.
 __device__ __forceinline__ void store_rec(TreeRec* dst, const TreeRec& r) {
     __stcs(reinterpret_cast<int4*>(dst), make_int4(static_cast<int>(r.info), r.ref, r.ref2, static_cast<int>(r.pad)));
+}
+
+// Per-CTA share of the residue-table pool: CTA b allocates from
+// [b * cap / grid, (b + 1) * cap / grid) with a shared-memory counter (no
+// global atomics; tables that do not fit become FULL records).
+struct PoolRegion {
+    uint32_t* next;  // shared
+    uint32_t end;
+};
+
+// Resolve a tree whose root walk stopped at clock node `w0` into its record,
+// one lane per job, depth-first: the clock node's children are walked
+// row-only to their next event (leaf or clock node); a clock node at level
+// < 4 adds a test (its right child is pushed, the left one walked next), a
+// leaf is stored in its depth-4 slot.  One test between two leaves -> SM /
+// MEM (no table); tests on up to 3 levels -> TABLE (the depth-4 layout
+// compacted into one 128-byte slot); 4 levels -> TABLE4 (two slots); deeper
+// -> FULL (ref = the first clock node, per-clock traversal in the
+// accumulate kernel).  The walks between events run as an inner loop, so the
+// warp's lanes (each on its own job) handle their events together.
+template <bool kAllSmem>
+__device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCtx& c, const TreeSrc& s, const Walk& w0,
+                                               const PoolRegion& region) {
+    TreeRec r{0u, 0, 0, 0u};
+    const uint2 t0 = test_mk(w0);
+    // Pending right children, a stack of at most 4: (byte offset << 8) | leaf << 7 | heap position.
+    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
+    int nst = 1;
+    st0 = (static_cast<uint32_t>(wchild(w0.fc) + 8) << 8) | (static_cast<uint32_t>((w0.fc >> 1) & 1) << 7) | 2u;
+    Walk cur = child_walk<kAllSmem>(c, s, w0, 0);
+    uint32_t P = 1;
+    // The table is built in the 128-byte RTRec form and moved to the
+    // two-slot RTRec4 form only when a fourth test level appears (rare).
+    RTRec4* q = nullptr;
+    bool big = false;
+    uint32_t tmask = 1u, idx = 0;
+    int maxlev = 0;
+    int32_t lleaf = -1;
+    // One leaf store in flight: its value load overlaps the next walk.
+    double* pend_dst = nullptr;
+    double pend_v = 0.0;
+    auto put_leaf = [&](uint32_t pos, int32_t leaf_idx) {
+        if (pend_dst) *pend_dst = pend_v;
+        const uint32_t lev = 31u - __clz(pos + 1u);
+        const uint32_t path = pos + 1u - (1u << lev);
+        pend_dst = big ? &q->leaf[path << (4u - lev)] : &reinterpret_cast<RTRec*>(q)->leaf[path << (3u - lev)];
+        pend_v = __ldg(&c.gnodes[leaf_idx].v);
+    };
+    while (true) {
+        while (cur.fc >= 0) {  // row-only steps to the next event
+            const int32_t x = rank_value(c, cur.fc);
+            const int right = x <= cur.key ? 0 : 1;
+            const int32_t nn = wchild(cur.fc) + 8 * right;
+            if ((cur.fc >> right) & 1) {
+                cur = Walk{nn, s.groot + (nn >> 3), kLeafFc};
+            } else {
+                cur.n = nn;
+                load_wnode<kAllSmem>(c, s, cur);
+            }
+        }
+        if (wfeat(cur.fc) == kFeatLeaf) {
+            if (!q) {
+                if (P == 1u) {
+                    lleaf = cur.key;
+                } else {  // P == 2 with no table: one test between two leaves
+                    r.info = (wfeat(w0.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w0.key) << 16);
+                    r.ref = lleaf;
+                    r.ref2 = cur.key;
+                    return r;
+                }
+            } else {
+                put_leaf(P, cur.key);
+            }
+            if (nst == 0) break;
+            const uint32_t e = st0;
+            st0 = st1;
+            st1 = st2;
+            st2 = st3;
+            --nst;
+            P = e & 127u;
+            const int32_t n = static_cast<int32_t>(e >> 8);
+            if ((e >> 7) & 1u) {
+                cur = Walk{n, s.groot + (n >> 3), kLeafFc};
+            } else {
+                cur = Walk{n, 0, 0};
+                load_wnode<kAllSmem>(c, s, cur);
+            }
+            continue;
+        }
+        // A clock node at heap position P.
+        const int lev = 31 - __clz(static_cast<int>(P) + 1);
+        if (lev >= GD_RES_LEVELS || (!q && (idx = atomicAdd(region.next, 2u)) + 2u > region.end)) {
+            if (pend_dst) *pend_dst = pend_v;
+            r.info = kRecFull;
+            r.ref = s.groot + (w0.n >> 3);
+            return r;
+        }
+        if (!q) {
+            q = reinterpret_cast<RTRec4*>(p.pool + idx);
+            q->test[0] = t0;
+            if (lleaf >= 0) put_leaf(1u, lleaf);
+        }
+        if (lev == 3 && !big) {  // fourth level: depth-3 leaf slot k becomes depth-4 slot 2k
+            if (pend_dst) *pend_dst = pend_v;
+            pend_dst = nullptr;
+            RTRec* t = reinterpret_cast<RTRec*>(q);
+            double lv[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) lv[k] = t->leaf[k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q->leaf[2 * k] = lv[k];
+            big = true;
+        }
+        q->test[P] = test_mk(cur);
+        tmask |= 1u << P;
+        maxlev = max(maxlev, lev);
+        st3 = st2;
+        st2 = st1;
+        st1 = st0;
+        st0 = (static_cast<uint32_t>(wchild(cur.fc) + 8) << 8) | (static_cast<uint32_t>((cur.fc >> 1) & 1) << 7) |
+              (2u * P + 2u);
+        ++nst;
+        cur = child_walk<kAllSmem>(c, s, cur, 0);
+        P = 2u * P + 1u;
+    }
+    if (pend_dst) *pend_dst = pend_v;
+    const uint32_t D = static_cast<uint32_t>(maxlev) + 1u;  // 2, 3 or 4
+    // Leaves above the last level sit under always-left tests.
+#pragma unroll
+    for (uint32_t k = 1; k < 15; ++k) {
+        if (k + 1u < (1u << D) && !((tmask >> k) & 1u)) q->test[k] = make_uint2(0u, 0u);
+        if (k == 6 && D < 4) break;
+    }
+    r.ref = static_cast<int32_t>(idx);
+    if (big) {
+        r.info = kRecTable4;
+        return r;
+    }
+    reinterpret_cast<RTRec*>(q)->depth = D;
+    r.info = kRecTable;
+    return r;
 }
 
 // A root walk that stopped at a clock node, queued for resolution so the
@@ -377,14 +448,14 @@ struct Job {
 };
 constexpr int kJobCap = 64;
 
-// Lanes take queued jobs [0, min(32, count)) and write their records, then
-// the queue's tail moves to the front.
+// Every queued job is resolved (lane l takes jobs l, l + 32), then the queue
+// is empty.  Out of line: it is reached from every walk-group width and the
+// drain, and one copy of the residue code keeps the kernel in the I-cache.
 template <bool kAllSmem>
-__device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
-                                         int& count, int lane, TreeRec* out, int64_t tile0) {
-    const int take = min(32, count);
-    if (lane < take) {
-        const Job j = jobs[lane];
+__device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
+                                         int& count, int lane, TreeRec* out, int64_t tile0, const PoolRegion& region) {
+    for (int k = lane; k < count; k += 32) {
+        const Job j = jobs[k];
         WalkCtx c = c0;
         c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * 2);
         const int4 te = table[j.e];  // shared: no global round trip before the residue walk
@@ -395,16 +466,10 @@ __device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0,
         s.saddr = static_cast<uint32_t>(te.w);
         Walk w{j.n, 0, 0};
         load_wnode<kAllSmem>(c, s, w);
-        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_residue<kAllSmem>(p, c, s, w));
+        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_dfs<kAllSmem>(p, c, s, w, region));
     }
     __syncwarp();
-    const int rest = count - take;
-    Job mv;
-    if (lane < rest) mv = jobs[take + lane];
-    __syncwarp();
-    if (lane < rest) jobs[lane] = mv;
-    __syncwarp();
-    count = rest;
+    count = 0;
 }
 
 // Queue the walk of one tree if it stopped at a clock node, else store its
@@ -412,20 +477,23 @@ __device__ __forceinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0,
 template <bool kAllSmem>
 __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const WalkCtx& c, const int4* table, Job* jobs,
                                             int& count, int lane, bool v, const Walk& w, int32_t t, int32_t e,
-                                            int li, int model, TreeRec* out, int64_t tile0) {
+                                            int li, int model, TreeRec* out, int64_t tile0, const PoolRegion& region) {
     const bool job = v && wfeat(w.fc) != kFeatLeaf;
     if (v && !job) store_rec(out + rec_index(t, tile0 + li, p.n_apps), TreeRec{kRecConst, w.key, 0, 0u});
     const unsigned m = __ballot_sync(kFull, job);
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, e, li};
     count += __popc(m);
     __syncwarp();
-    if (count >= 32) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0);
+    if (count >= 32) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0, region);
 }
 
 constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
 constexpr int kMaxTileApps = 512;  // apps per walk tile (16 groups of 32)
 #ifndef GD_WALK_NW
 #define GD_WALK_NW 4  // independent walks per lane in the root-walk loop
+#endif
+#ifndef GD_WALK_ADAPT
+#define GD_WALK_ADAPT 1  // narrower walk groups for a stage's last trees
 #endif
 
 // One stage of the CTA's schedule.
@@ -582,6 +650,10 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     unsigned char* after_ranks = smem + 128 + NB * buf_bytes + walk_rank_bytes(p.n_cols, TA);
     Job* jobs = reinterpret_cast<Job*>(after_ranks) + warp * kJobCap;
     int4* tables = reinterpret_cast<int4*>(after_ranks + walk_jobs_bytes(blockDim.x >> 5));
+    uint32_t* pool_next = reinterpret_cast<uint32_t*>(tables + NB * kStageTrees);
+    PoolRegion region;
+    region.next = pool_next;
+    region.end = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x + 1) * p.pool_cap / gridDim.x);
     WTRACE(0);
     const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
     const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
@@ -597,6 +669,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
                              tables + b * kStageTrees, desc + b);
     };
     if (threadIdx.x == 0) {
+        *pool_next = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * p.pool_cap / gridDim.x);
         for (int b = 0; b < NB; ++b) {
             mbar_init(bar0 + 8 * b, 1);
             mbar_init(bar0 + 32 + 8 * b, nwarps);
@@ -669,17 +742,21 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         const int32_t nt = p.n_trees[ii.model];
         TreeRec* out = p.rec[ii.model];
         int count = 0;
-        // This warp walks the stage's trees t = 2*q0 + sub + NSUB*k, NW side by side.
+        // This warp walks the stage's trees t = 2*q0 + sub + NSUB*k, up to
+        // NW side by side; a stage with fewer trees left (e.g. one pair of
+        // configs[3]'s depth-12 trees) takes a narrower group so no walk
+        // slot idles.
         const int4* table = tables + buf * kStageTrees;
         constexpr int NW = GD_WALK_NW;
         const int32_t t_last = min(2 * s.q1, nt) - 1;
-        for (int32_t t0 = 2 * s.q0 + sub; t0 <= t_last; t0 += NW * NSUB) {
-            TreeSrc src[NW];
-            int32_t tt[NW];
-            bool vv[NW];
-            Walk w[NW];
+        auto group = [&](int32_t t0, auto nw_tag) {
+            constexpr int G = decltype(nw_tag)::value;
+            TreeSrc src[G];
+            int32_t tt[G];
+            bool vv[G];
+            Walk w[G];
 #pragma unroll
-            for (int h = 0; h < NW; ++h) {
+            for (int h = 0; h < G; ++h) {
                 tt[h] = t0 + NSUB * h;
                 vv[h] = valid && tt[h] <= t_last;
                 const int4 e = table[min(tt[h], t_last) - 2 * s.q0];
@@ -690,15 +767,25 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
                 w[h] = Walk{0, 0, 0};
                 load_wnode<kAllSmem>(c, src[h], w[h]);
             }
-            walkn<kAllSmem, NW>(c, src, vv, w);
+            walkn<kAllSmem, G>(c, src, vv, w);
 #pragma unroll
-            for (int h = 0; h < NW; ++h)
+            for (int h = 0; h < G; ++h)
                 finish_walk<kAllSmem>(p, c0, c, table, jobs, count, lane, vv[h], w[h], tt[h],
                                       min(tt[h], t_last) - 2 * s.q0, li, ii.model,
-                                      out, tile0);
-        }
+                                      out, tile0, region);
+        };
+        int32_t t0 = 2 * s.q0 + sub;
+#if GD_WALK_ADAPT
+        for (; t0 + NSUB * (NW - 1) <= t_last; t0 += NW * NSUB) group(t0, std::integral_constant<int, NW>{});
+#else
+        for (; t0 <= t_last; t0 += NW * NSUB) group(t0, std::integral_constant<int, NW>{});
+#endif
+        const int32_t rest = t0 <= t_last ? (t_last - t0) / NSUB + 1 : 0;  // warp-uniform
+        if (rest > 2) group(t0, std::integral_constant<int, NW>{});
+        else if (rest == 2) group(t0, std::integral_constant<int, 2>{});
+        else if (rest == 1) group(t0, std::integral_constant<int, 1>{});
         if (k == 0) WTRACE(4);
-        if (count > 0) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0);
+        if (count > 0) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0, region);
         if (k == 0) WTRACE(5);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`
@@ -889,7 +976,7 @@ struct RingT {
     static constexpr int kRv = kVal + (RS + 1) * 32 * 8;
     static constexpr int kSideOff = kRv + (RS + 1) * 32 * 8;
     static constexpr int kOvf = kSideOff + (RS + 1) * kSide * 128;
-    static constexpr int kRow = kOvf + 128;
+    static constexpr int kRow = kOvf + 256;
     __host__ __device__ static constexpr int rs(int g) { return g % (RR + 1); }  // record slot
     __host__ __device__ static constexpr int ss(int g) { return g % (RS + 1); }  // side slot
 };
@@ -944,7 +1031,9 @@ struct AccModel {
 };
 
 // Full per-candidate traversal from node n (grid nodes) with a packed clock:
-// predict_row on the substituted row (models.cpp:71-78).
+// predict_row on the substituted row (models.cpp:71-78).  (Walking all CPL
+// clocks in lockstep, inline or out of line, costs the hot loop registers:
+// spills, +40 % accumulate time at configs[3].)
 __device__ __forceinline__ double eval_full_packed(const PNode* __restrict__ nodes, int32_t n, const double* row,
                                                    unsigned ck) {
     const double sm = static_cast<double>(ck >> 16), mem = static_cast<double>(ck & 0xffffu);
@@ -1016,7 +1105,7 @@ __device__ __forceinline__ void add_table(double (&acc)[CPL], const unsigned (&c
             const uint2 t = lds_u2(sb + n * 8u);
             n = 2u * n + 1u + ((ck[i] & t.x) > t.y ? 1u : 0u);
         }
-        acc[i] = __dadd_rn(acc[i], lds_f64(sb + 64u + (n - ((1u << D) - 1u)) * 8u));
+        acc[i] = __dadd_rn(acc[i], lds_f64(sb + 64u + ((n - ((1u << D) - 1u)) << (3 - D)) * 8u));
     }
 }
 
@@ -1032,15 +1121,15 @@ __device__ __forceinline__ void add_table2_mem_uniform(double (&acc)[CPL], const
     if (t0.x != 0xffffffffu) {  // root resolved per lane: child n, then one test per clock
         const uint32_t n = 1u + ((mem_l & t0.x) > t0.y ? 1u : 0u);
         const uint2 tc = lds_u2(sb + n * 8u);
-        const double lv = lds_f64(sb + 64u + (2u * n - 2u) * 8u), rv = lds_f64(sb + 64u + (2u * n - 1u) * 8u);
+        const double lv = lds_f64(sb + 64u + (2u * n - 2u) * 16u), rv = lds_f64(sb + 64u + (2u * n - 1u) * 16u);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & tc.x) > tc.y ? rv : lv);
         return;
     }
     const uint2 t1 = lds_u2(sb + 8u), t2 = lds_u2(sb + 16u);
     if (t1.x != 0xffffffffu && t2.x != 0xffffffffu) {  // both children resolved per lane: one test per clock
-        const double lv = lds_f64(sb + 64u + ((mem_l & t1.x) > t1.y ? 8u : 0u));
-        const double rv = lds_f64(sb + 80u + ((mem_l & t2.x) > t2.y ? 8u : 0u));
+        const double lv = lds_f64(sb + 64u + ((mem_l & t1.x) > t1.y ? 16u : 0u));
+        const double rv = lds_f64(sb + 96u + ((mem_l & t2.x) > t2.y ? 16u : 0u));
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] > t0.y ? rv : lv);
         return;
@@ -1105,9 +1194,32 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
             add_table<CPL, 3>(acc, ck, sb);
         }
     } else {
+        const uint32_t info = lds_u32(ws + RG::kMeta + slotb);
         const int32_t ref = static_cast<int32_t>(lds_u32(ws + RG::kMeta + slotb + 4));
+        if ((info & 7u) == kRecTable4) {  // rare: copied on demand (two pool slots)
+            const uint32_t sb = ws + RG::kOvf;
+            __syncwarp();
+            if (lane < 16) {
+                const int4 x = __ldg(reinterpret_cast<const int4*>(pool + ref) + lane);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * lane), "r"(x.x), "r"(x.y),
+                             "r"(x.z), "r"(x.w)
+                             : "memory");
+            }
+            __syncwarp();
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, ref, row, ck[i]));
+            for (int i = 0; i < CPL; ++i) {
+                uint32_t n = 0;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const uint2 t = lds_u2(sb + n * 8u);
+                    n = 2u * n + 1u + ((ck[i] & t.x) > t.y ? 1u : 0u);
+                }
+                acc[i] = __dadd_rn(acc[i], lds_f64(sb + 128u + (n - 15u) * 8u));
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], eval_full_packed(m.nodes, ref, row, ck[i]));
+        }
     }
 }
 
@@ -1734,7 +1846,7 @@ WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 
     for (int groups = 16; groups >= 1; groups >>= 1) {
         if (groups > max_groups) continue;
         const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(g.n_subs * groups) +
-                             static_cast<size_t>(g.n_bufs) * kStageTrees * 16;
+                             static_cast<size_t>(g.n_bufs) * kStageTrees * 16 + 16;
         if (fixed + g.n_bufs * 8 * 4 > kLimit) continue;
         int64_t stage = static_cast<int64_t>((kLimit - fixed) / (8 * g.n_bufs)) & ~1;
         if (stage > 16384) stage = 16384;
@@ -1760,10 +1872,11 @@ int64_t env_i64(const char* name, int64_t dflt) {
     return e ? std::atoll(e) : dflt;
 }
 
-// Residue-table capacity per app: 1/4 of the trees (GDVFS_POOL_DIV overrides
-// the divisor; overflowing tables fall back to FULL records).
+// Residue-table pool slots per app: 1/3 of the trees (a table takes two
+// slots while it is built; GDVFS_POOL_DIV overrides the divisor; tables that
+// do not fit fall back to FULL records).
 int64_t pool_per_app(const GridParams& p) {
-    int64_t div = env_i64("GDVFS_POOL_DIV", 4);
+    int64_t div = env_i64("GDVFS_POOL_DIV", 3);
     if (div < 1) div = 1;
     return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 1;
 }
@@ -1775,11 +1888,12 @@ bool acc_sliced(int64_t n_apps) {
     return f >= 0 ? f != 0 : n_apps <= 256;
 }
 
-// Apps per batch: the walk records of one batch stay bounded (and, at the
-// default budget, mostly L2-resident between the two kernels).
+// Apps per batch: the walk -> accumulate hand-off of one batch (records,
+// residue tables, ranks) is bounded by a scratch budget (4 GiB; it streams
+// through HBM -- beyond a few thousand apps it does not stay in L2).
 int64_t batch_apps(const GridParams& p) {
     const int64_t per_app = grid_scratch_per_app(p);
-    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 31);
+    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 32);
     int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
     b = b < 256 ? 256 : b;
     return b < p.n_apps ? b : p.n_apps;

@@ -121,6 +121,13 @@ int parse_model_file(const char* path, gd_model& m);
 int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid* g, const gd_select_opts* o,
                      gd_decision* out, double* e_out, double* t_out, gd_decision** keep_dev_out);
 
+// fit_gbt's booster on the device (gd_train.cu): fills the forest arrays in
+// fit_gbt's node order and the base prediction.
+int fit_gbt_device(gd_ctx* ctx, const double* rows, int64_t n, int32_t p, const double* targets,
+                   const gd_gbt_config& cfg, std::vector<int64_t>& offsets, std::vector<int32_t>& feature,
+                   std::vector<double>& threshold, std::vector<int32_t>& left, std::vector<int32_t>& right,
+                   std::vector<double>& leaf, double& base);
+
 // A device copy of `src` (any model holding its host arrays) on ctx's device
 // (gd_capi.cpp; used by gd_multi_model_replicate).
 int clone_model(gd_ctx* ctx, const gd_model* src, gd_model** out);

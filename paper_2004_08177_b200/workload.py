@@ -352,6 +352,157 @@ def make_scenario(name: str, n_apps: int, catalog, n_trees: int, depth: int, see
     return Scenario(name, fe, ft, grid, seed, cols, (lo, hi))
 
 
+# ---- trained models -----------------------------------------------------------
+#
+# The synthetic ensembles above are random trees with a fixed clock-split
+# rate.  The scenario below instead TRAINS both ensembles (fit_gbt on the GPU,
+# the reference's exact booster) on profiled records of a roofline
+# application model, the shape of the reference's synthetic GPU
+# (synthdata.cpp: time = max(compute / sm, memory / mem) + stall, power from
+# the utilisations, counters proportional to the work, throughputs = counter /
+# time, a binned utilisation as a categorical column, clock-keyed
+# distractors).  Trained trees split on the clock columns wherever the target
+# depends on them -- near the root, with the distribution of clock residues a
+# production model has.
+
+
+def _archetypes(n: int, seed: int):
+    r = np.random.default_rng(seed)
+    return dict(cw=r.uniform(420.0, 5300.0, n), mw=r.uniform(70.0, 1950.0, n), stall=r.uniform(0.10, 1.40, n),
+                kc=r.uniform(0.034, 0.105, n), km=r.uniform(0.007, 0.058, n), gain=r.uniform(0.7, 1.3, (n, 16)),
+                key=r.integers(0, 2**31, n))
+
+
+def _profiles(arch, idx, sm, mem):
+    """Profiled rows (the 50-column schema), energy and time for app idx x
+    clocks (sm, mem) (flat arrays of equal length)."""
+    cw, mw, st = arch["cw"][idx], arch["mw"][idx], arch["stall"][idx]
+    g = arch["gain"][idx]
+    smf, memf = sm.astype(np.float64), mem.astype(np.float64)
+    tc, tm = cw / smf, mw / memf
+    t_det = np.maximum(tc, tm) + st
+    uc, um = tc / t_det, tm / t_det
+    stall_frac = st / t_det
+    volt = 0.70 + 0.35 * (smf - 135.0) / 1800.0
+    power = 30.0 + arch["kc"][idx] * smf * volt * volt * uc + arch["km"][idx] * memf * um
+    rows = np.zeros((len(idx), N_COLS))
+    counters = [cw * 250.0, cw * 620.0, cw * 45.0, cw * 110.0, cw * 55.0, mw * 31250.0, mw * 1.0e6, mw * 11000.0,
+                mw * 48000.0, mw * 26000.0, mw * 8000.0 + cw * 900.0, mw * 7.3e5, (cw + mw) * 1800.0,
+                (cw + mw) * 2600.0]
+    free = [c for c in range(N_COLS) if c not in CAT_COLS and c not in (SM_COL, MEM_COL)]
+    k = 0
+    for j, c in enumerate(counters):
+        rows[:, free[k]] = c * g[:, j % 16]
+        k += 1
+    for j, c in enumerate(counters[:8]):  # throughputs: counter / time
+        rows[:, free[k]] = c * g[:, (j + 3) % 16] / t_det / 1e9
+        k += 1
+    for v in (100.0 * uc, 4.0 * uc * (1 - 0.6 * stall_frac), 100.0 * (1 - 0.55 * um), 100.0 * (0.55 + 0.45 * uc),
+              100.0 * stall_frac * 0.55, 100.0 * np.minimum(1.0, 0.5 * um), 0.03 + 0.12 * um,
+              8.0 * uc * (1 - 0.5 * stall_frac)):
+        rows[:, free[k]] = v
+        k += 1
+    while k < len(free):  # distractors keyed by (app, clock)
+        h = (arch["key"][idx] * 1000003 + sm * 7919 + mem * 104729 + k * 15485863) % 1000003
+        rows[:, free[k]] = 100.0 * h / 1000003.0
+        k += 1
+    rows[:, SM_COL], rows[:, MEM_COL] = smf, memf
+    lvl_u = np.minimum((um * 4).astype(int), 3)  # binned utilisations (categorical levels)
+    lvl_c = np.minimum((uc * 4).astype(int), 3)
+    time = t_det * (1.0 + 0.01 * np.sin(arch["key"][idx] + smf))
+    energy = power * time
+    return rows, (lvl_c, lvl_u), energy, time
+
+
+def make_trained_scenario(name: str, n_apps: int, catalog, n_trees: int, depth: int, seed: int = 1234,
+                          train_apps: int = 48, stride: int = 3, ctx=None,
+                          app_range: Optional[tuple] = None) -> Scenario:
+    """(apps, catalog, E/T ensembles TRAINED on profiled records with the
+    GPU fit_gbt).  Training set: `train_apps` archetypes x every `stride`-th
+    catalog clock; categorical levels encoded by their mean target per
+    target (so the time model sees its own values, cat_t).  Query rows: the
+    default-clock (max sm, max mem) profile of `n_apps` further archetypes."""
+    import paper_2004_08177_b200 as gd
+
+    if isinstance(catalog, str):
+        sm, mem = CATALOGS[catalog]()
+    else:
+        sm, mem = (np.ascontiguousarray(x, dtype=np.int32) for x in catalog)
+    lo, hi = app_range if app_range is not None else (0, n_apps)
+    arch = _archetypes(train_apps + n_apps, seed)
+    ci = np.arange(0, sm.shape[0], stride)
+    ia = np.repeat(np.arange(train_apps), ci.shape[0])
+    ic = np.tile(ci, train_apps)
+    rows, (lc, lu), energy, time = _profiles(arch, ia, sm[ic], mem[ic])
+    enc = {}
+    for tgt, y in ((0, energy), (1, time)):
+        vals = []
+        for lv in (lc, lu):
+            m = np.array([y[lv == k].mean() if np.any(lv == k) else y.mean() for k in range(4)])
+            vals.append(m)
+        enc[tgt] = vals
+    def encode(r, lvls, tgt):
+        out = r.copy()
+        for ci_, (c, lv) in enumerate(zip(CAT_COLS, lvls)):
+            out[:, c] = enc[tgt][ci_][lv]
+        return out
+    xe, xt = encode(rows, (lc, lu), 0), encode(rows, (lc, lu), 1)
+    me = gd.fit_gbt(xe, energy, n_trees, depth, 0.1, 3.0, seed, 0, ctx=ctx)
+    mt = gd.fit_gbt(xt, time, n_trees, depth, 0.1, 3.0, seed, 1, ctx=ctx)
+    fe, ft = me.export(), mt.export()
+    me.close()
+    mt.close()
+    qa = np.arange(train_apps + lo, train_apps + hi)
+    d_sm, d_mem = np.full(hi - lo, int(sm.max()), np.int32), np.full(hi - lo, int(mem.max()), np.int32)
+    qrows, (qc, qu), _, _ = _profiles(arch, qa, d_sm, d_mem)
+    q_e = encode(qrows, (qc, qu), 0)
+    q_t = encode(qrows, (qc, qu), 1)
+    cat_t = np.ascontiguousarray(q_t[:, list(CAT_COLS)])
+    grid = GridInputs(np.ascontiguousarray(q_e), cat_t, np.array(CAT_COLS, dtype=np.int32), sm, mem, SM_COL, MEM_COL)
+    return Scenario(name, fe, ft, grid, seed, None, (lo, hi))
+
+
+def record_kinds(forest: Forest, rows: np.ndarray, sm_col: int, mem_col: int, max_apps: int = 64) -> dict:
+    """Share of (app, tree) pairs per walk-record kind (what the walk kernel
+    emits): CONST (row-only walk ends on a leaf), SM / MEM (one clock test
+    between two leaves), TABLE (2-3 test levels), TABLE4 (4), FULL (deeper).
+    CPU analysis over the first `max_apps` rows -- a measurement aid."""
+    off, f, th, le, ri = forest.tree_offsets, forest.feature, forest.threshold, forest.left, forest.right
+
+    def walk(o, n, row):
+        while True:
+            ft = f[o + n]
+            if ft < 0 or ft == sm_col or ft == mem_col:
+                return n
+            n = le[o + n] if row[ft] <= th[o + n] else ri[o + n]
+
+    def levels(o, n, row):  # test levels of the clock-only residue below node n
+        n = walk(o, n, row)
+        if f[o + n] < 0:
+            return 0
+        return 1 + max(levels(o, le[o + n], row), levels(o, ri[o + n], row))
+
+    counts = dict(CONST=0, SM=0, MEM=0, TABLE=0, TABLE4=0, FULL=0)
+    n_apps = min(max_apps, rows.shape[0])
+    for a in range(n_apps):
+        row = rows[a]
+        for t in range(forest.n_trees):
+            o = int(off[t])
+            d = levels(o, 0, row)
+            if d == 0:
+                counts["CONST"] += 1
+            elif d == 1:
+                counts["SM" if f[o + walk(o, 0, row)] == sm_col else "MEM"] += 1
+            elif d <= 3:
+                counts["TABLE"] += 1
+            elif d == 4:
+                counts["TABLE4"] += 1
+            else:
+                counts["FULL"] += 1
+    tot = max(1, n_apps * forest.n_trees)
+    return {k: round(v / tot, 4) for k, v in counts.items()}
+
+
 def deadlines_from_times(times: np.ndarray, seed: int, infeasible_frac: float = 0.05) -> np.ndarray:
     """Per-app relative deadline: a seeded quantile q ~ U(0.1, 0.9) of the app's own
     predicted times over the grid; `infeasible_frac` of apps
@@ -405,4 +556,6 @@ CONFIGS = {
     "c3": dict(n_apps=1_000_000, catalog="b200", n_trees=1000, depth=10),
     "c4": dict(n_apps=10_000_000, catalog="gtx980", n_trees=2000, depth=12),
     "c5": dict(n_apps=64, catalog="gtx980", n_trees=500, depth=8),
+    # configs[1] shape with ensembles TRAINED on profiled records (GPU fit_gbt)
+    "c2t": dict(n_apps=10_000, catalog="gtx980", n_trees=500, depth=8, trained=True),
 }

@@ -98,6 +98,10 @@ def ref() -> Optional[C.CDLL]:
         r.ref_c1_scenario.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.c_int, C.c_int, C.c_int]
         r.ref_truth_oracle.argtypes = [C.c_uint64, P, P, P, P, P]
+        r.ref_c1_train.argtypes = [C.c_uint64, C.c_int, C.c_int, P, P, P, P]
+        r.ref_fit_gbt.argtypes = [P, C.c_int64, C.c_int, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64,
+                                  C.c_int, P, P, P]
+        r.ref_fit_gbt_export.argtypes = [P, P, P, P, P, P]
         r.ref_bench_grid.restype = C.c_double
         r.ref_bench_grid.argtypes = [C.POINTER(ForestView), C.c_double, C.c_double, C.POINTER(ForestView),
                                      C.c_double, C.c_double, P, C.c_int, P, P, C.c_int, C.c_int64, P, P, C.c_int32,
@@ -195,6 +199,32 @@ def ref_predict(forest, rows):
     _ref_check(ref().ref_predict_forest(C.byref(fv), forest.base, forest.learning_rate, forest.target, _p(rows),
                                         rows.shape[0], rows.shape[1], _p(out)))
     return out
+
+
+def ref_c1_train(seed=7, stride=2, target=0):
+    """The C1 catalog's encoded training matrix (rows, targets) from the reference."""
+    n, p = C.c_int64(), C.c_int32()
+    _ref_check(ref().ref_c1_train(seed, stride, target, None, None, C.byref(n), C.byref(p)))
+    rows = np.empty((n.value, p.value), np.float64)
+    targets = np.empty(n.value, np.float64)
+    _ref_check(ref().ref_c1_train(seed, stride, target, _p(rows), _p(targets), C.byref(n), C.byref(p)))
+    return rows, targets
+
+
+def ref_fit_gbt(rows, targets, iterations, depth, lr=0.1, l2=3.0, seed=7, target=0):
+    """models::fit_gbt on (rows, targets): the Forest in fit_gbt's own node order."""
+    from paper_2004_08177_b200.workload import Forest
+
+    rows = np.ascontiguousarray(rows, np.float64)
+    targets = np.ascontiguousarray(targets, np.float64)
+    nt, nn, base = C.c_int32(), C.c_int64(), C.c_double()
+    _ref_check(ref().ref_fit_gbt(_p(rows), rows.shape[0], rows.shape[1], _p(targets), iterations, depth, lr, l2, seed,
+                                 target, C.byref(nt), C.byref(nn), C.byref(base)))
+    off = np.empty(nt.value + 1, np.int64)
+    f, l, r = (np.empty(nn.value, np.int32) for _ in range(3))
+    th, lv = np.empty(nn.value, np.float64), np.empty(nn.value, np.float64)
+    _ref_check(ref().ref_fit_gbt_export(_p(off), _p(f), _p(th), _p(l), _p(r), _p(lv)))
+    return Forest(off, f, th, l, r, lv, base.value, lr, target, rows.shape[1])
 
 
 def ref_save_forest(forest, path):

@@ -259,6 +259,23 @@ KNOBS = {
 }
 
 
+@pytest.mark.parametrize("w_clk,depth", [(0.25, 11), (0.4, 9), (0.15, 12)])
+def test_k2_deep_residues_tables4_and_full(ctx, w_clk, depth):
+    # clock-heavy deep trees: residues with 3-4 test levels (TABLE / TABLE4
+    # records) and deeper ones (FULL), in both accumulate modes
+    sc = W.make_scenario("deep_res", 300, "gtx980", 40, depth, seed=int(100 * w_clk) + depth, w_clk=w_clk)
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=5)
+    want, we, wt = O.oracle_grid(sc.energy, sc.time, sc.grid, budgets)
+    for n in (300, 60):  # 60 apps: the sliced (latency) accumulate
+        g = W.GridInputs(sc.grid.rows[:n], sc.grid.cat_t[:n], sc.grid.cat_cols, sc.grid.sm, sc.grid.mem,
+                         sc.grid.sm_col, sc.grid.mem_col)
+        got, ge, gt = gd.grid_select(me, mt, g, budgets[:n], return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we[:n])) and np.array_equal(bits(gt), bits(wt[:n]))
+        assert decisions_equal(got, want[:n])
+
+
 @pytest.mark.parametrize("knob", list(KNOBS))
 def test_k2_internal_paths_vs_oracle(ctx, knob, monkeypatch):
     for k, v in KNOBS[knob].items():
