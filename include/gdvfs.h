@@ -194,6 +194,14 @@ int gd_predict_rows_device(gd_ctx* ctx, const gd_model* model, const double* d_r
  * selection of scheduler.cpp:54-100,212-223 per app.  e_out / t_out
  * (A x C, nullable) receive the per-candidate predictions (what the
  * ClockPredictor of make_model_predictor returns). */
+/* Shapes: any catalog size (above 512 clocks the kernels run in 512-clock
+ * chunks and one wide selection); models or catalogs the partial-evaluation
+ * pipeline cannot take -- a feature with more than 65535 distinct
+ * thresholds, a tree of more than 65536 nodes, clock values above 65535 MHz,
+ * or per-clock records (rec_of_clock) -- run on the general per-candidate
+ * kernel, with the same results.  gd_grid_select_device cannot read the
+ * catalog on the host: its clock values must lie in 1..65535 MHz unless
+ * rec_of_clock is given. */
 int gd_grid_select(gd_ctx* ctx, const gd_model* energy, const gd_model* time, const gd_grid* grid,
                    const gd_select_opts* opts, gd_decision* out, double* e_out, double* t_out);
 int gd_grid_select_device(gd_ctx* ctx, const gd_model* energy, const gd_model* time, const gd_grid* d_grid,

@@ -266,9 +266,7 @@ int validate_grid(const gd_model* me, const gd_model* mt, const gd_grid* g, cons
         return set_error(GD_ERR_INVALID_ARGUMENT, "predict: column mismatch between grid rows and models");
     }
     if (g->n_cols <= 0 || g->n_cols > gd::kMaxCols) return set_error(GD_ERR_UNSUPPORTED, "grid_select: bad column count");
-    if (g->n_clocks <= 0 || g->n_clocks > gd::kMaxClocks) {
-        return set_error(GD_ERR_UNSUPPORTED, "grid_select: clock catalog must hold 1..512 clocks");
-    }
+    if (g->n_clocks <= 0) return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: empty clock catalog");
     if (g->n_apps < 0 || g->n_records < 0 || g->n_cat < 0 || g->n_cat > g->n_cols) {
         return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: negative sizes");
     }
@@ -336,16 +334,8 @@ void timing_mark(void* user, const char* name) {
     ctx->marks.push_back(name);
 }
 
-// begin_timing: false when the caller already opened the timing interval list
-// (the host-buffer path marks its copies around the kernels).
-int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
-              gd_decision* d_out, double* d_e, double* d_t, const double* d_rows_t, bool begin_timing = true) {
-    const bool general = g.rec_of_clock != nullptr;
-    if (!general) {
-        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col);
-        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col);
-        if (rc) return rc;
-    }
+gd::GridParams grid_params(const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
+                           bool general) {
     gd::GridParams p{};
     p.e_nodes = general ? me->d_nodes : me->d_grid_nodes;
     p.e_roots = me->d_roots;
@@ -373,16 +363,12 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.t_base = mt->base;
     p.t_lr = mt->lr;
     p.rows = g.rows;
-    p.rows_t = d_rows_t;
     p.cat_t = g.cat_t;
     p.cat_cols = g.cat_cols;
     p.rec_of_clock = g.rec_of_clock;
     p.sm = g.sm_clock;
     p.mem = g.mem_clock;
     p.budgets = g.budgets;
-    p.out = d_out;
-    p.e_out = d_e;
-    p.t_out = d_t;
     p.n_apps = g.n_apps;
     p.n_cols = g.n_cols;
     p.n_cat = g.n_cat;
@@ -392,19 +378,101 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.mode = o.mode;
     p.objective = o.objective;
     p.best_effort = o.best_effort;
+    p.out_stride = g.n_clocks;
+    return p;
+}
+
+// Whether a call takes the partial-evaluation pipeline: no per-clock records
+// (rec_of_clock), catalog clocks that pack into 16 bits (force_general
+// otherwise), and models the walk handles (gd::grid_fast_path_ok).  Every
+// other shape runs the general per-candidate kernel -- on the GPU, never an
+// error.
+bool takes_fast_path(const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
+                     bool force_general) {
+    if (g.rec_of_clock || force_general) return false;
+    return gd::grid_fast_path_ok(grid_params(me, mt, g, o, true));
+}
+
+// begin_timing: false when the caller already opened the timing interval list
+// (the host-buffer path marks its copies around the kernels).  Catalogs wider
+// than gd::kMaxClocks run in 512-clock chunks that write the E/T tables
+// (row stride = the full catalog), then one wide selection.
+int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
+              gd_decision* d_out, double* d_e, double* d_t, bool begin_timing = true, bool force_general = false) {
     if (g.n_apps == 0) return GD_OK;
-    Scratch s{ctx->stream, &ctx->pbuf[0]};
-    const size_t bytes = gd::grid_scratch_bytes(p, general);
-    const size_t i_scr = s.add(bytes);
-    GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
+    const bool general = !takes_fast_path(me, mt, g, o, force_general);
+    if (!general) {
+        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col);
+        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col);
+        if (rc) return rc;
+    }
+    gd::GridParams p = grid_params(me, mt, g, o, general);
+    p.out = d_out;
+    p.e_out = d_e;
+    p.t_out = d_t;
+    const int64_t A = g.n_apps, C = g.n_clocks;
+    const bool wide = C > gd::kMaxClocks;
+    // General mode reads per-record time rows (the categorical columns
+    // replaced by their time encoding); wide mode needs the full tables.
+    Scratch side{ctx->stream};
+    const size_t i_rt = side.add(general && g.n_records > 0 ? static_cast<size_t>(g.n_records) * g.n_cols * sizeof(double) : 0);
+    const size_t i_we = side.add(wide && !d_e ? static_cast<size_t>(A) * C * sizeof(double) : 0);
+    const size_t i_wt = side.add(wide && !d_t ? static_cast<size_t>(A) * C * sizeof(double) : 0);
+    const size_t i_wd = side.add(wide ? static_cast<size_t>(A) * sizeof(gd_decision) : 0);
+    GD_CUDA(side.alloc(), "cudaMallocAsync(grid side buffers)");
+    if (general && g.n_records > 0) {
+        p.rows_t = static_cast<double*>(side.ptr(i_rt));
+        int e = gd::launch_build_rows_t(g.rows, g.cat_t, g.cat_cols, g.n_cat, g.n_records, g.n_cols,
+                                        const_cast<double*>(p.rows_t), ctx->stream);
+        ++ctx->launches;
+        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
+    }
     gd::LaunchMark mark = nullptr;
     if (ctx->timing) {
         if (begin_timing) timing_begin(ctx);
         mark = timing_mark;
     }
-    int e = gd::launch_grid_select(p, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches, mark,
-                                   ctx);
-    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");
+    auto run = [&](const gd::GridParams& q) -> int {
+        Scratch s{ctx->stream, &ctx->pbuf[0]};
+        const size_t bytes = gd::grid_scratch_bytes(q, general);
+        const size_t i_scr = s.add(bytes);
+        GD_CUDA(s.alloc(), "cudaMallocAsync(grid scratch)");
+        int e = gd::launch_grid_select(q, general, ctx->sm_count, ctx->stream, s.ptr(i_scr), bytes, &ctx->launches,
+                                       mark, ctx);
+        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "grid kernel launch");
+        return GD_OK;
+    };
+    if (!wide) return run(p);
+    double* E = d_e ? d_e : static_cast<double*>(side.ptr(i_we));
+    double* T = d_t ? d_t : static_cast<double*>(side.ptr(i_wt));
+    for (int64_t c0 = 0; c0 < C; c0 += gd::kMaxClocks) {
+        gd::GridParams q = p;
+        q.n_clocks = static_cast<int32_t>(C - c0 < gd::kMaxClocks ? C - c0 : gd::kMaxClocks);
+        q.sm = g.sm_clock + c0;
+        q.mem = g.mem_clock + c0;
+        if (g.rec_of_clock) q.rec_of_clock = g.rec_of_clock + c0;
+        q.e_out = E + c0;
+        q.t_out = T + c0;
+        q.out = static_cast<gd_decision*>(side.ptr(i_wd));  // per-chunk choices are discarded
+        q.out_stride = C;
+        int rc = run(q);
+        if (rc) return rc;
+    }
+    gd::SelectParams sp{};
+    sp.energy = E;
+    sp.time = T;
+    sp.sm = g.sm_clock;
+    sp.budgets = g.budgets;
+    sp.out = d_out;
+    sp.n_apps = A;
+    sp.n_clocks = static_cast<int32_t>(C);
+    sp.mode = o.mode;
+    sp.objective = o.objective;
+    sp.best_effort = o.best_effort;
+    int e = gd::launch_select_wide(sp, ctx->sm_count, ctx->stream);
+    ++ctx->launches;
+    if (mark) mark(ctx, "select");
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "select kernel launch");
     return GD_OK;
 }
 
@@ -759,18 +827,7 @@ int gd_grid_select_device(gd_ctx* ctx, const gd_model* me, const gd_model* mt, c
     if ((rc = check_model(ctx, me, "grid_select")) || (rc = check_model(ctx, mt, "grid_select"))) return rc;
     if ((rc = validate_grid(me, mt, g, o))) return rc;
     if (!d_out) return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: null decisions");
-    const double* rows_t = nullptr;
-    Scratch s{ctx->stream};
-    if (g->rec_of_clock && g->n_records > 0) {
-        const size_t i_rt = s.add(static_cast<size_t>(g->n_records) * g->n_cols * sizeof(double));
-        GD_CUDA(s.alloc(), "cudaMallocAsync");
-        rows_t = static_cast<double*>(s.ptr(i_rt));
-        int e = gd::launch_build_rows_t(g->rows, g->cat_t, g->cat_cols, g->n_cat, g->n_records, g->n_cols,
-                                        const_cast<double*>(rows_t), ctx->stream);
-        ++ctx->launches;
-        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
-    }
-    return grid_impl(ctx, me, mt, *g, *o, d_out, d_e, d_t, rows_t);
+    return grid_impl(ctx, me, mt, *g, *o, d_out, d_e, d_t);
 }
 
 }  // extern "C"
@@ -835,7 +892,7 @@ void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
         ok = cudaMemcpyAsync(dev_in, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
-        ok = ok && grid_impl(ctx, me, mt, dg, o, host_out ? host_out : dev_out, nullptr, nullptr, nullptr, false) == GD_OK;
+        ok = ok && grid_impl(ctx, me, mt, dg, o, host_out ? host_out : dev_out, nullptr, nullptr, false) == GD_OK;
         if (!host_out) {
             ok = ok &&
                  cudaMemcpyAsync(ctx->out_stage, dev_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
@@ -878,13 +935,12 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     }
     if (g->n_apps == 0) return GD_OK;
     const int64_t A = g->n_apps, R = g->n_records, C = g->n_clocks;
+    bool force_general = false;
     for (int64_t c = 0; c < C; ++c) {
         if (g->sm_clock[c] <= 0 || g->mem_clock[c] <= 0) {
             return set_error(GD_ERR_INVALID_ARGUMENT, "grid_select: clock frequencies must be positive");
         }
-        if (g->sm_clock[c] > 65535 || g->mem_clock[c] > 65535) {
-            return set_error(GD_ERR_UNSUPPORTED, "grid_select: clock frequencies above 65535 MHz");
-        }
+        if (g->sm_clock[c] > 65535 || g->mem_clock[c] > 65535) force_general = true;  // no 16-bit clock keys
     }
     for (int32_t k = 0; k < g->n_cat; ++k) {
         if (g->cat_cols[k] < 0 || g->cat_cols[k] >= g->n_cols) {
@@ -909,9 +965,9 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     const size_t i_out = s.add(static_cast<size_t>(A) * sizeof(gd_decision));
     const size_t i_e = s.add(e_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
     const size_t i_t = s.add(t_out ? static_cast<size_t>(A) * C * sizeof(double) : 0);
-    const size_t i_rt = s.add(g->rec_of_clock ? static_cast<size_t>(R) * g->n_cols * sizeof(double) : 0);
     const size_t in_end0 = s.pieces[i_bud].first + s.pieces[i_bud].second;
-    const bool graphable = graphs_enabled() && !keep_dev_out && !ctx->timing && !g->rec_of_clock && !e_out && !t_out &&
+    const bool graphable = graphs_enabled() && !keep_dev_out && !ctx->timing && !e_out && !t_out &&
+                           takes_fast_path(me, mt, *g, *o, force_general) && C <= gd::kMaxClocks &&
                            in_end0 <= kStageLimit && static_cast<size_t>(A) * sizeof(gd_decision) <= kStageLimit;
     gd_graph_entry key;
     key.me = me->uid;
@@ -1017,16 +1073,8 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     dg.mem_clock = static_cast<int32_t*>(s.ptr(i_mem));
     dg.budgets = static_cast<double*>(s.ptr(i_bud));
     if (ctx->timing) timing_mark(ctx, "h2d");
-    const double* rows_t = nullptr;
-    if (g->rec_of_clock) {
-        rows_t = static_cast<double*>(s.ptr(i_rt));
-        int e = gd::launch_build_rows_t(dg.rows, dg.cat_t, dg.cat_cols, dg.n_cat, R, dg.n_cols,
-                                        const_cast<double*>(rows_t), ctx->stream);
-        ++ctx->launches;
-        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "rows_t kernel");
-    }
     rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
-                   static_cast<double*>(s.ptr(i_t)), rows_t, false);
+                   static_cast<double*>(s.ptr(i_t)), false, force_general);
     if (rc) return rc;
     if (keep_dev_out) {
         *keep_dev_out = static_cast<gd_decision*>(s.ptr(i_out));
@@ -1064,7 +1112,7 @@ int gd_select(gd_ctx* ctx, const double* energy, const double* time, int64_t n_a
               int32_t n_clocks, const double* budgets, const gd_select_opts* o, gd_decision* out) {
     int rc = activate(ctx);
     if (rc) return rc;
-    if (!o || n_apps < 0 || n_clocks <= 0 || n_clocks > gd::kMaxClocks ||
+    if (!o || n_apps < 0 || n_clocks <= 0 ||
         (n_apps > 0 && (!energy || !time || !sm_clock || !budgets || !out))) {
         return set_error(GD_ERR_INVALID_ARGUMENT, "gd_select: bad arguments");
     }

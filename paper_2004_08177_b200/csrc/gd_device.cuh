@@ -83,6 +83,7 @@ struct GridParams {
     int64_t n_apps;
     int32_t n_cols, n_cat, n_clocks, sm_col, mem_col;
     int32_t mode, objective, best_effort;
+    int64_t out_stride;  // row stride of e_out / t_out (n_clocks, or the full catalog for a clock chunk)
 };
 
 struct SelectParams {
@@ -116,6 +117,12 @@ typedef void (*LaunchMark)(void* user, const char* name);
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
                        size_t scratch_bytes, int64_t* launches, LaunchMark mark = nullptr, void* user = nullptr);
 int launch_select(const SelectParams& p, int sm_count, void* stream);
+// K3 for catalogs wider than kMaxClocks: a warp per app striding over the clocks.
+int launch_select_wide(const SelectParams& p, int sm_count, void* stream);
+// Whether the partial-evaluation pipeline (rank -> walk -> accumulate) can
+// take these models: 16-bit feature ranks, trees of <= 65536 nodes and a
+// walk geometry that fits shared memory.  Otherwise the general kernel runs.
+bool grid_fast_path_ok(const GridParams& p);
 int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream);
 // Selection frontier (gd_kernels.cu frontier_kernel): sorted times, prefix
 // best catalog index, first (best-effort) index or -2 for non-finite rows.

@@ -140,6 +140,7 @@ struct AccParams {
     int32_t n_apps;
     int32_t n_cols, n_cat, n_clocks;
     int32_t mode, objective, best_effort;
+    int64_t out_stride;  // row stride of e_out / t_out
     // Sliced mode (small batches): per-app E/T staging and arrival counters.
     double* et;          // [n_apps][2][n_clocks]
     uint32_t* arrive;    // [n_apps], zeroed
@@ -1573,8 +1574,8 @@ __global__ void __launch_bounds__(kAccThreads, (CPL >= 12 ? 4 : GD_ACC_MIN_BLOCK
                 const int c = map[i * 32 + lane];
                 cidx[i] = c;
                 if (c >= 0) {
-                    if (p.e_out) p.e_out[a * p.n_clocks + c] = E[i];
-                    if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
+                    if (p.e_out) p.e_out[a * p.out_stride + c] = E[i];
+                    if (p.t_out) p.t_out[a * p.out_stride + c] = T[i];
                 }
             }
             select_epilogue<CPL>(E, T, smv, cidx, lane, __ldg(p.budgets + a), p.mode, p.objective, p.best_effort,
@@ -1635,7 +1636,7 @@ __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __gr
             const double t = finish(p.base[1], p.lr[1], acc[0]);
             if (c < C) {
                 et[C + c] = t;
-                if (p.t_out) p.t_out[a * C + c] = t;
+                if (p.t_out) p.t_out[a * p.out_stride + c] = t;
             }
             __threadfence();
             pair_sync_a(pair);  // both warps of the pair have published their slice
@@ -1644,7 +1645,7 @@ __global__ void __launch_bounds__(kAccThreads) grid_acc_sliced_kernel(const __gr
             const double e = clamp_energy(finish(p.base[0], p.lr[0], acc[0]));
             if (c < C) {
                 et[c] = e;
-                if (p.e_out) p.e_out[a * C + c] = e;
+                if (p.e_out) p.e_out[a * p.out_stride + c] = e;
             }
             __threadfence();
             pair_sync_a(pair);
@@ -1696,7 +1697,7 @@ __global__ void __launch_bounds__(256) grid_general_kernel(const __grid_constant
         for (int i = 0; i < CPL; ++i) {
             accE[i] = accT[i] = 0.0;
             const int c = lane * CPL + i;
-            const int64_t rec = c < p.n_clocks ? (p.rec_of_clock ? __ldg(p.rec_of_clock + a * p.n_clocks + c) : a) : 0;
+            const int64_t rec = c < p.n_clocks ? (p.rec_of_clock ? __ldg(p.rec_of_clock + a * p.out_stride + c) : a) : 0;
             rE[i] = p.rows + rec * F;
             rT[i] = p.rows_t + rec * F;
         }
@@ -1719,8 +1720,8 @@ __global__ void __launch_bounds__(256) grid_general_kernel(const __grid_constant
             T[i] = finish(p.t_base, p.t_lr, accT[i]);
             const int c = lane * CPL + i;
             if (c < p.n_clocks) {
-                if (p.e_out) p.e_out[a * p.n_clocks + c] = E[i];
-                if (p.t_out) p.t_out[a * p.n_clocks + c] = T[i];
+                if (p.e_out) p.e_out[a * p.out_stride + c] = E[i];
+                if (p.t_out) p.t_out[a * p.out_stride + c] = T[i];
             }
         }
         int cidx[CPL];
@@ -1901,6 +1902,10 @@ int64_t batch_apps(const GridParams& p) {
 
 }  // namespace
 
+bool grid_fast_path_ok(const GridParams& p) {
+    return p.rank16 && p.max_tree_nodes <= 65536 && walk_geom(p, batch_apps(p)).warps > 0;
+}
+
 int64_t grid_scratch_per_app(const GridParams& p) {
     const int64_t pairs = ((p.e_trees + 1) >> 1) + ((p.t_trees + 1) >> 1);
     const int64_t pool = pool_per_app(p);  // residue tables per app
@@ -1961,7 +1966,8 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const WalkGeom small = walk_geom(p, B, 56 * 1024);
         if (small.warps > 0) wg = small;
     }
-    // 16-bit ranks and tree-local child indices bound what the walk handles.
+    // 16-bit ranks and tree-local child indices bound what the walk handles
+    // (grid_fast_path_ok routes other models to the general kernel).
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_wint + 1) & ~1) <= wg.win_nodes;
     auto walk_kern = all_smem ? grid_walk_kernel<true> : grid_walk_kernel<false>;
@@ -2067,6 +2073,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         a.mode = p.mode;
         a.objective = p.objective;
         a.best_effort = p.best_effort;
+        a.out_stride = p.out_stride;
         if (sliced) {
             a.et = et;
             a.arrive = arrive;

@@ -198,6 +198,80 @@ __global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ Sel
     }
 }
 
+// K3 for catalogs wider than a warp's CPL <= 16 register layout (> 512
+// clocks): a warp per app, lane l takes clocks l, l + 32, ...  Text mode and
+// the best-effort fallback are argmins of a total key (same rules as
+// select_epilogue); literal mode is select_literal's order-dependent scan,
+// run by lane 0 over the whole row.
+__global__ void __launch_bounds__(256) select_wide_kernel(const __grid_constant__ SelectParams p) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const int64_t C = p.n_clocks;
+    for (int64_t a = static_cast<int64_t>(blockIdx.x) * wpb + warp; a < p.n_apps;
+         a += static_cast<int64_t>(gridDim.x) * wpb) {
+        const double* E = p.energy + a * C;
+        const double* T = p.time + a * C;
+        const double budget = __ldg(p.budgets + a);
+        Cand best;
+        best.idx = -1;
+        best.obj = best.t = best.e = 0.0;
+        best.sm = 0;
+        if (p.mode == GD_MODE_TEXT) {
+            for (int64_t c = lane; c < C; c += 32) {
+                const double t = __ldg(T + c), e = __ldg(E + c);
+                if (t > budget) continue;
+                Cand k{objective_value(e, t, p.objective), t, e, __ldg(p.sm + c), static_cast<int>(c)};
+                if (text_less(k, best)) best = k;
+            }
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) {
+                Cand o = shfl_cand(best, m);
+                if (text_less(o, best)) best = o;
+            }
+        } else {
+            if (lane == 0) {  // scheduler.cpp:86-100
+                double min_objective = DBL_MAX, max_time = budget;
+                for (int64_t c = 0; c < C; ++c) {
+                    const double e = __ldg(E + c), t = __ldg(T + c);
+                    const double value = objective_value(e, t, p.objective);
+                    if (value < min_objective && t <= max_time) {
+                        min_objective = value;
+                        max_time = t;
+                        best.idx = static_cast<int>(c);
+                        best.e = e;
+                        best.t = t;
+                    }
+                }
+            }
+            best.idx = __shfl_sync(kFull, best.idx, 0);
+            best.e = __shfl_sync(kFull, best.e, 0);
+            best.t = __shfl_sync(kFull, best.t, 0);
+        }
+        int note = GD_NOTE_NONE;
+        if (best.idx < 0 && p.best_effort) {
+            for (int64_t c = lane; c < C; c += 32) {
+                Cand k{0.0, __ldg(T + c), __ldg(E + c), __ldg(p.sm + c), static_cast<int>(c)};
+                if (fast_less(k, best)) best = k;
+            }
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) {
+                Cand o = shfl_cand(best, m);
+                if (fast_less(o, best)) best = o;
+            }
+            note = GD_NOTE_BEST_EFFORT;
+        }
+        if (lane == 0) {
+            gd_decision d;
+            d.clock_index = best.idx;
+            d.status = best.idx >= 0 ? GD_SCHEDULED : GD_REJECTED;
+            d.note = best.idx >= 0 ? note : GD_NOTE_NONE;
+            d.energy_ws = best.idx >= 0 ? best.e : 0.0;
+            d.time_s = best.idx >= 0 ? best.t : 0.0;
+            p.out[a] = d;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Selection frontier (the remaining_time EDF loop's per-job query, SURVEY
 // §8f #2): per app, the candidates sorted by (T, E, catalog index) and the
@@ -472,7 +546,16 @@ int launch_dadd_probe(double* scratch, int blocks, int iters, void* stream) {
     return cudaGetLastError();
 }
 
+int launch_select_wide(const SelectParams& p, int sm_count, void* stream) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, select_wide_kernel, 256, 0);
+    const int blocks = grid_blocks(8, p.n_apps, sm_count, per_sm);
+    select_wide_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+    return cudaGetLastError();
+}
+
 int launch_select(const SelectParams& p, int sm_count, void* stream) {
+    if (p.n_clocks > kMaxClocks) return launch_select_wide(p, sm_count, stream);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int cpl = (p.n_clocks + 31) / 32;
     if (cpl <= 1) return launch_select_cpl<1>(p, sm_count, s);

@@ -549,3 +549,64 @@ def test_sum_tolerance_statement():
     # The kernels are bit-exact; north_star's 1e-5 relative tolerance is the
     # documented ceiling and is implied by 0-ulp equality above.
     assert REL_TOL == 1e-5
+
+
+# ---- shapes outside the partial-evaluation pipeline: general kernel / chunked catalogs ----
+
+def _check_vs_oracle(ctx, sc, grid=None, combos=((0, 0, 0), (1, 1, 1))):
+    grid = grid or sc.grid
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, grid, np.ones(grid.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=4)
+    for mode, obj, be in combos:
+        opts = gd.SchedulerOptions(mode=["text", "literal"][mode], budget="full", objective=["energy", "power"][obj],
+                                   best_effort_fallback=bool(be))
+        want, we, wt = O.oracle_grid(sc.energy, sc.time, grid, budgets, mode, obj, be)
+        got, ge, gt = gd.grid_select(me, mt, grid, budgets, opts, return_predictions=True)
+        assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+        assert decisions_equal(got, want)
+        only = gd.grid_select(me, mt, grid, budgets, opts)
+        assert decisions_equal(only, want)
+
+
+@pytest.mark.parametrize("general", [False, True])
+def test_wide_catalog_600_clocks(ctx, general):
+    pairs = [(300 + 10 * i, m) for m in (405, 810, 2600, 3505, 5000, 6000) for i in range(100)]
+    sm, mem = W._sorted_catalog(pairs)
+    assert sm.shape[0] == 600
+    sc = W.make_scenario("wide", 40, (sm, mem), 30, 6, seed=8, w_clk=0.2)
+    grid = sc.grid
+    if general:
+        rng = np.random.default_rng(3)
+        grid = W.GridInputs(grid.rows, grid.cat_t, grid.cat_cols, grid.sm, grid.mem, grid.sm_col, grid.mem_col,
+                            rec_of_clock=rng.integers(0, 40, size=(40, 600)).astype(np.int32))
+    _check_vs_oracle(ctx, sc, grid)
+    # K3 alone over the same wide tables
+    _, e, t = O.oracle_grid(sc.energy, sc.time, grid, np.full(40, 5.0))
+    for mode in ("text", "literal"):
+        opts = gd.SchedulerOptions(mode=mode, budget="full", best_effort_fallback=True)
+        got = gd.select(e, t, grid.sm, np.full(40, 5.0), opts, ctx=ctx)
+        want = O.oracle_select(e, t, grid.sm, np.full(40, 5.0), mode=int(mode == "literal"), best_effort=1)
+        assert decisions_equal(got, want)
+
+
+def test_clocks_above_16_bits_take_general_kernel(ctx):
+    sm, mem = W._sorted_catalog([(70000 + 500 * i, 90000) for i in range(20)] + [(1000 + 10 * i, 405) for i in range(8)])
+    sc = W.make_scenario("ghz", 50, (sm, mem), 25, 6, seed=2, w_clk=0.3)
+    _check_vs_oracle(ctx, sc)
+
+
+def test_many_thresholds_and_huge_trees_take_general_kernel(ctx):
+    # > 65535 distinct thresholds on one feature (no 16-bit ranks) ...
+    sc = W.make_scenario("thr", 30, "gtx980", 300, 8, seed=6, w_clk=0.05)
+    rng = np.random.default_rng(0)
+    for f in (sc.energy, sc.time):
+        internal = (f.feature >= 0) & (f.feature != W.SM_COL) & (f.feature != W.MEM_COL)
+        f.feature[internal] = 7
+        f.threshold[internal] = sc.grid.rows[:, 7].mean() * np.exp(rng.uniform(-1, 1, int(internal.sum())))
+    assert np.unique(sc.energy.threshold[sc.energy.feature == 7]).shape[0] > 65535
+    _check_vs_oracle(ctx, sc)
+    # ... and a tree of more than 65536 nodes (depth 16)
+    big = W.make_scenario("big", 12, "p100", 2, 16, seed=3, w_clk=0.05)
+    assert big.energy.n_nodes // 2 > 65536
+    _check_vs_oracle(ctx, big, combos=((0, 0, 0),))
