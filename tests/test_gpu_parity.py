@@ -5,6 +5,7 @@ clocks, statuses) must be identical; predictions are compared bit-for-bit
 which tests/test_gpu_parity.py::test_sum_tolerance_statement documents).
 """
 import itertools
+import os
 
 import numpy as np
 import pytest
@@ -523,26 +524,72 @@ def test_c2_full_size_properties(ctx):
 
 @pytest.mark.parametrize("shape", ["c3", "c4"])
 def test_deep_config_shapes_sampled_vs_oracle(ctx, shape):
-    # BASELINE configs[2] / configs[3] tree shapes (1000 trees depth 10 on the
-    # 200-clock B200 grid; 2000 trees depth 12 on the 267-clock grid) at a
-    # reduced app count: windowed walks, deep residues; seeded apps against
-    # the oracle bit for bit, the rest through the properties.
-    if shape == "c3":
-        sc, sample = W.make_scenario("c3s", 512, "b200", 1000, 10, seed=4), 6
-    else:
-        sc, sample = W.make_scenario("c4s", 256, "gtx980", 2000, 12, seed=3), 2
+    # BASELINE configs[2] / configs[3] at their full tree shapes (1000 trees
+    # depth 10 on the 200-clock B200 grid; 2000 trees depth 12 on the
+    # 267-clock grid), on slices of the very batches bench.py times (the same
+    # chunk-seeded rows: apps [lo, hi) of the 1M / 10M-app batch).  128 apps
+    # bit for bit against the REFERENCE's own predict + select (oracle/_ref,
+    # all host threads) -- or 16 against the C oracle where _ref is absent --
+    # and every app through the properties.
+    cfg = W.CONFIGS[shape]
+    lo = 7 * W.CHUNK_APPS + 123  # inside the batch, across a chunk boundary
+    n = 2048 if shape == "c3" else 1024
+    sc = W.make_scenario("bench", cfg["n_apps"], cfg["catalog"], cfg["n_trees"], cfg["depth"], seed=1234,
+                         chunked=True, app_range=(lo, lo + n))
     me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
     _, e, t = gd.grid_select(me, mt, sc.grid, np.ones(sc.grid.n_apps), return_predictions=True)
     budgets = W.deadlines_from_times(t, seed=6)
     d1, e1, t1 = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
     assert np.array_equal(bits(e1), bits(e)) and np.array_equal(bits(t1), bits(t))
     assert decisions_equal(O.oracle_select(e1, t1, sc.grid.sm, budgets), d1)
-    idx = np.random.default_rng(1).choice(sc.grid.n_apps, sample, replace=False)
+    sample = 128 if O.ref_available() else 16
+    idx = np.sort(np.random.default_rng(1).choice(sc.grid.n_apps, sample, replace=False))
     sub = W.GridInputs(sc.grid.rows[idx], sc.grid.cat_t[idx], sc.grid.cat_cols, sc.grid.sm, sc.grid.mem, W.SM_COL,
                        W.MEM_COL)
-    want, we, wt = O.oracle_grid(sc.energy, sc.time, sub, budgets[idx])
+    if O.ref_available():
+        _, want, we, wt = O.ref_bench_grid(sc.energy, sc.time, sub, budgets[idx], sample, os.cpu_count() or 1, tables=True)
+    else:
+        want, we, wt = O.oracle_grid(sc.energy, sc.time, sub, budgets[idx])
     assert np.array_equal(bits(e1[idx]), bits(we)) and np.array_equal(bits(t1[idx]), bits(wt))
     assert decisions_equal(d1[idx], want)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_c2_every_app_vs_reference(ctx):
+    # BASELINE configs[1] at full size, EVERY one of the 10k apps against the
+    # reference's own models::predict + schedule_d_dvfs (oracle/_ref, all
+    # host threads): E/T tables and decisions bit for bit.
+    sc = W.make_scenario("c2", **W.CONFIGS["c2"])
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t = gd.grid_select(me, mt, sc.grid, np.ones(sc.grid.n_apps), return_predictions=True)
+    budgets = W.deadlines_from_times(t, seed=3)
+    got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
+    _, want, we, wt = O.ref_bench_grid(sc.energy, sc.time, sc.grid, budgets, sc.grid.n_apps, os.cpu_count() or 1,
+                                              tables=True)
+    assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+    assert decisions_equal(got, want)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_trained_models_fast_path_vs_reference(ctx):
+    # Ensembles TRAINED with the GPU fit_gbt on profiled records (clock
+    # splits where the targets depend on the clocks, near the roots) through
+    # the partial-evaluation path, against the reference's predict + select.
+    sc = W.make_trained_scenario("trained", 600, "gtx980", 120, 8, seed=5, train_apps=24, stride=5, ctx=ctx)
+    kinds = W.record_kinds(sc.time, sc.grid.rows, sc.grid.sm_col, sc.grid.mem_col, max_apps=16)
+    assert kinds["CONST"] < 0.95  # the clock columns do matter to these models
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t = gd.grid_select(me, mt, sc.grid, np.ones(sc.grid.n_apps), return_predictions=True)
+    budgets = W.deadlines_from_times(t, seed=8)
+    for opts in (gd.SchedulerOptions(budget="full"), gd.SchedulerOptions(budget="full", objective="power")):
+        got, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, opts, return_predictions=True)
+        _, want, we, wt = O.ref_bench_grid(sc.energy, sc.time, sc.grid, budgets, sc.grid.n_apps, os.cpu_count() or 1,
+                                              tables=True)
+        assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+        if opts.objective == "energy":
+            assert decisions_equal(got, want)
+        else:
+            assert decisions_equal(got, O.oracle_select(we, wt, sc.grid.sm, budgets, objective=1))
 
 
 def test_sum_tolerance_statement():
