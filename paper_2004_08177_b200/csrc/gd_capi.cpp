@@ -358,6 +358,7 @@ gd::GridParams grid_params(const gd_model* me, const gd_model* mt, const gd_grid
     p.e_thr_off = me->d_thr_off;
     p.t_thr_off = mt->d_thr_off;
     p.rank16 = me->max_thr_per_feature <= 65535 && mt->max_thr_per_feature <= 65535;
+    p.rank8 = me->max_thr_per_feature <= 255 && mt->max_thr_per_feature <= 255;
     p.t_roots = mt->d_roots;
     p.t_trees = mt->n_trees();
     p.t_base = mt->base;

@@ -68,6 +68,7 @@ struct GridParams {
     const int32_t* t_wint;
     int32_t max_wint;
     int32_t rank16;  // every feature has <= 65535 distinct thresholds (16-bit ranks)
+    int32_t rank8;   // ... <= 255 (8-bit ranks: 1024-app walk tiles)
 
     const double* rows;    // [n_records, n_cols] energy-encoded
     const double* rows_t;  // [n_records, n_cols] time-encoded (general mode only)

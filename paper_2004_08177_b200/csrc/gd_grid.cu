@@ -153,7 +153,7 @@ struct WalkParams {
     const int32_t* wint[2];    // per tree: loadable walk-node prefix (window size when it fits)
     const PNode* gnodes[2];    // grid nodes (leaf values)
     int32_t n_trees[2];
-    const uint16_t* ranks;     // [2][n_apps][n_cols] for the batch
+    const unsigned char* ranks;  // [2][tile][n_cols][tile_apps] ranks of RB bytes for the batch
     int32_t n_apps;            // apps in the batch
     int32_t n_cols;
     int32_t tile_apps;         // apps per work item = 32 * groups
@@ -221,10 +221,23 @@ __device__ __forceinline__ void load_wnode(const WalkCtx& c, const TreeSrc& s, W
     }
 }
 
-__device__ __forceinline__ int32_t rank_value(const WalkCtx& c, int32_t fc) {
-    uint16_t x;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(c.row_saddr + static_cast<uint32_t>(wfeat(fc) * c.row_stride)));
+// The rank of feature wfeat(fc) for the app whose ranks start at shared
+// address `row` (RB = bytes per rank: 1 when every feature of both models has
+// at most 255 distinct thresholds, else 2).
+template <int RB>
+__device__ __forceinline__ int32_t rank_at(uint32_t row, int32_t stride, int32_t fc) {
+    const uint32_t a = row + static_cast<uint32_t>(wfeat(fc) * stride);
+    uint32_t x;
+    if constexpr (RB == 1) {
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(x) : "r"(a));
+    } else {
+        asm volatile("ld.shared.u16 %0, [%1];" : "=r"(x) : "r"(a));
+    }
     return static_cast<int32_t>(x);
+}
+template <int RB>
+__device__ __forceinline__ int32_t rank_value(const WalkCtx& c, int32_t fc) {
+    return rank_at<RB>(c.row_saddr, c.row_stride, fc);
 }
 
 // N independent row-only walks advanced in lockstep until each reaches a leaf
@@ -233,8 +246,9 @@ __device__ __forceinline__ int32_t rank_value(const WalkCtx& c, int32_t fc) {
 // synthesizes it -- {leaf position, packed index = grid root + position,
 // kLeafFc} -- instead of loading it; lanes that do not advance reload the
 // root (always in the window) so the loop stays branch-free.
-template <bool kAllSmem, int N>
-__device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], const bool (&v)[N], Walk (&w)[N]) {
+template <bool kAllSmem, int RB, int N>
+__device__ __forceinline__ void walkn(const WalkCtx& c, const uint32_t (&ra)[N], const TreeSrc (&s)[N],
+                                      const bool (&v)[N], Walk (&w)[N]) {
     bool g[N];
     bool any = false;
 #pragma unroll
@@ -245,7 +259,7 @@ __device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], c
     while (any) {
         int32_t x[N];
 #pragma unroll
-        for (int h = 0; h < N; ++h) x[h] = rank_value(c, g[h] ? w[h].fc : 0);
+        for (int h = 0; h < N; ++h) x[h] = rank_at<RB>(ra[h], c.row_stride, g[h] ? w[h].fc : 0);
         any = false;
 #pragma unroll
         for (int h = 0; h < N; ++h) {
@@ -263,16 +277,6 @@ __device__ __forceinline__ void walkn(const WalkCtx& c, const TreeSrc (&s)[N], c
             any |= g[h];
         }
     }
-}
-
-template <bool kAllSmem>
-__device__ __forceinline__ void walk2(const WalkCtx& c, const TreeSrc& s, bool va, Walk& a, bool vb, Walk& b) {
-    const TreeSrc ss[2] = {s, s};
-    const bool vv[2] = {va, vb};
-    Walk ww[2] = {a, b};
-    walkn<kAllSmem, 2>(c, ss, vv, ww);
-    a = ww[0];
-    b = ww[1];
 }
 
 // Compare key of a clock node's test (see the header comment).
@@ -316,7 +320,7 @@ struct PoolRegion {
 // -> FULL (ref = the first clock node, per-clock traversal in the
 // accumulate kernel).  The walks between events run as an inner loop, so the
 // warp's lanes (each on its own job) handle their events together.
-template <bool kAllSmem>
+template <bool kAllSmem, int RB>
 __device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCtx& c, const TreeSrc& s, const Walk& w0,
                                                const PoolRegion& region) {
     TreeRec r{0u, 0, 0, 0u};
@@ -346,7 +350,7 @@ __device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCt
     };
     while (true) {
         while (cur.fc >= 0) {  // row-only steps to the next event
-            const int32_t x = rank_value(c, cur.fc);
+            const int32_t x = rank_value<RB>(c, cur.fc);
             const int right = x <= cur.key ? 0 : 1;
             const int32_t nn = wchild(cur.fc) + 8 * right;
             if ((cur.fc >> right) & 1) {
@@ -452,13 +456,13 @@ constexpr int kJobCap = 64;
 // Every queued job is resolved (lane l takes jobs l, l + 32), then the queue
 // is empty.  Out of line: it is reached from every walk-group width and the
 // drain, and one copy of the residue code keeps the kernel in the I-cache.
-template <bool kAllSmem>
+template <bool kAllSmem, int RB>
 __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
                                          int& count, int lane, TreeRec* out, int64_t tile0, const PoolRegion& region) {
     for (int k = lane; k < count; k += 32) {
         const Job j = jobs[k];
         WalkCtx c = c0;
-        c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * 2);
+        c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * RB);
         const int4 te = table[j.e];  // shared: no global round trip before the residue walk
         TreeSrc s;
         s.wroot = te.x;
@@ -467,7 +471,7 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
         s.saddr = static_cast<uint32_t>(te.w);
         Walk w{j.n, 0, 0};
         load_wnode<kAllSmem>(c, s, w);
-        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_dfs<kAllSmem>(p, c, s, w, region));
+        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_dfs<kAllSmem, RB>(p, c, s, w, region));
     }
     __syncwarp();
     count = 0;
@@ -475,17 +479,17 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
 
 // Queue the walk of one tree if it stopped at a clock node, else store its
 // constant record; run a round of jobs once 32 are pending.
-template <bool kAllSmem>
-__device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const WalkCtx& c, const int4* table, Job* jobs,
+template <bool kAllSmem, int RB>
+__device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
                                             int& count, int lane, bool v, const Walk& w, int32_t t, int32_t e,
-                                            int li, int model, TreeRec* out, int64_t tile0, const PoolRegion& region) {
+                                            int li, TreeRec* out, int64_t tile0, const PoolRegion& region) {
     const bool job = v && wfeat(w.fc) != kFeatLeaf;
     if (v && !job) store_rec(out + rec_index(t, tile0 + li, p.n_apps), TreeRec{kRecConst, w.key, 0, 0u});
     const unsigned m = __ballot_sync(kFull, job);
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, e, li};
     count += __popc(m);
     __syncwarp();
-    if (count >= 32) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0, region);
+    if (count >= 32) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
 }
 
 constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
@@ -629,13 +633,18 @@ __device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int
 __host__ __device__ constexpr size_t walk_jobs_bytes(int warps) {
     return static_cast<size_t>(warps) * kJobCap * sizeof(Job);
 }
-__host__ __device__ constexpr size_t walk_rank_bytes(int n_cols, int tile_apps) {
-    return (static_cast<size_t>(n_cols) * tile_apps * 2 + 15) & ~static_cast<size_t>(15);
+__host__ __device__ constexpr size_t walk_rank_bytes(int n_cols, int tile_apps, int rb) {
+    return (static_cast<size_t>(n_cols) * tile_apps * rb + 15) & ~static_cast<size_t>(15);
 }
 
 // Grid: persistent CTAs; blockDim = 64 * groups (two warps per group of 32
 // apps, taking the even / odd trees of every stage).
-template <bool kAllSmem>
+//
+// RB = 1 (every feature of both models has <= 255 distinct thresholds):
+// 8-bit ranks, tiles of 1024 apps -- each warp walks two blocks of 32 apps
+// (lane = apps li and li + 512), so a stage's trees are staged once per 1024
+// apps and a lane has twice the walks in flight.
+template <bool kAllSmem, int RB>
 __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant__ WalkParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,8 +656,8 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     // descriptors at +64 (NB <= 4).
     Stage* desc = reinterpret_cast<Stage*>(smem + 64);
     const uint32_t bar0 = smem_addr(smem), bufs0 = smem_addr(smem + 128);
-    uint16_t* srank = reinterpret_cast<uint16_t*>(smem + 128 + NB * buf_bytes);
-    unsigned char* after_ranks = smem + 128 + NB * buf_bytes + walk_rank_bytes(p.n_cols, TA);
+    unsigned char* srank = smem + 128 + NB * buf_bytes;
+    unsigned char* after_ranks = smem + 128 + NB * buf_bytes + walk_rank_bytes(p.n_cols, TA, RB);
     Job* jobs = reinterpret_cast<Job*>(after_ranks) + warp * kJobCap;
     int4* tables = reinterpret_cast<int4*>(after_ranks + walk_jobs_bytes(blockDim.x >> 5));
     uint32_t* pool_next = reinterpret_cast<uint32_t*>(tables + NB * kStageTrees);
@@ -686,10 +695,10 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     // a contiguous, coalesced 16-byte copy) by threads [t0, blockDim.x).
     auto stage_ranks = [&](int32_t tile, int32_t model, int t0) {
         const int64_t tiles = (p.n_apps + TA - 1) / TA;
-        const int4* src =
-            reinterpret_cast<const int4*>(p.ranks + ((static_cast<int64_t>(model) * tiles + tile) * p.n_cols) * TA);
+        const int4* src = reinterpret_cast<const int4*>(
+            p.ranks + ((static_cast<int64_t>(model) * tiles + tile) * p.n_cols) * TA * RB);
         const uint32_t dst = smem_addr(srank);
-        const int n16 = p.n_cols * TA / 8;
+        const int n16 = p.n_cols * TA * RB / 16;
         // cp.async: every 16-byte piece in flight at once (a load -> store
         // loop would serialise one L2 round trip per iteration).
         for (int i = static_cast<int>(threadIdx.x) - t0; i >= 0 && i < n16; i += blockDim.x - t0) {
@@ -731,15 +740,14 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
             __syncthreads();
         }
 
+        // Lane apps: li (and li + 512 with 1024-app tiles).
+        constexpr int APL = RB == 1 ? 2 : 1;
         const int li = group * 32 + lane;
-        const bool valid = li < n_here;
         WalkCtx c0;  // rank base of the tile (jobs add their own app)
         c0.wnodes = p.wnodes[ii.model];
         c0.gnodes = p.gnodes[ii.model];
         c0.row_saddr = smem_addr(srank);
-        c0.row_stride = TA * 2;
-        WalkCtx c = c0;
-        c.row_saddr += static_cast<uint32_t>((valid ? li : 0) * 2);
+        c0.row_stride = TA * RB;
         const int32_t nt = p.n_trees[ii.model];
         TreeRec* out = p.rec[ii.model];
         int count = 0;
@@ -748,32 +756,37 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         // configs[3]'s depth-12 trees) takes a narrower group so no walk
         // slot idles.
         const int4* table = tables + buf * kStageTrees;
-        constexpr int NW = GD_WALK_NW;
+        constexpr int NW = GD_WALK_NW / APL;  // trees per group
         const int32_t t_last = min(2 * s.q1, nt) - 1;
+        // One group: trees t0, t0 + NSUB, ... (G / APL of them) for each of
+        // the lane's APL apps -- G independent walks.
         auto group = [&](int32_t t0, auto nw_tag) {
-            constexpr int G = decltype(nw_tag)::value;
+            constexpr int G = decltype(nw_tag)::value * APL;
             TreeSrc src[G];
+            uint32_t ra[G];
             int32_t tt[G];
+            int la[G];
             bool vv[G];
             Walk w[G];
 #pragma unroll
             for (int h = 0; h < G; ++h) {
-                tt[h] = t0 + NSUB * h;
-                vv[h] = valid && tt[h] <= t_last;
+                tt[h] = t0 + NSUB * (h / APL);
+                la[h] = li + 512 * (h % APL);
+                vv[h] = la[h] < n_here && tt[h] <= t_last;
+                ra[h] = c0.row_saddr + static_cast<uint32_t>((vv[h] ? la[h] : 0) * RB);
                 const int4 e = table[min(tt[h], t_last) - 2 * s.q0];
                 src[h].wroot = e.x;
                 src[h].groot = e.y;
                 src[h].win = kAllSmem ? 0xffffffffu : static_cast<uint32_t>(e.z);
                 src[h].saddr = static_cast<uint32_t>(e.w);
                 w[h] = Walk{0, 0, 0};
-                load_wnode<kAllSmem>(c, src[h], w[h]);
+                load_wnode<kAllSmem>(c0, src[h], w[h]);
             }
-            walkn<kAllSmem, G>(c, src, vv, w);
+            walkn<kAllSmem, RB, G>(c0, ra, src, vv, w);
 #pragma unroll
             for (int h = 0; h < G; ++h)
-                finish_walk<kAllSmem>(p, c0, c, table, jobs, count, lane, vv[h], w[h], tt[h],
-                                      min(tt[h], t_last) - 2 * s.q0, li, ii.model,
-                                      out, tile0, region);
+                finish_walk<kAllSmem, RB>(p, c0, table, jobs, count, lane, vv[h], w[h], tt[h],
+                                          min(tt[h], t_last) - 2 * s.q0, la[h], out, tile0, region);
         };
         int32_t t0 = 2 * s.q0 + sub;
 #if GD_WALK_ADAPT
@@ -783,10 +796,10 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
 #endif
         const int32_t rest = t0 <= t_last ? (t_last - t0) / NSUB + 1 : 0;  // warp-uniform
         if (rest > 2) group(t0, std::integral_constant<int, NW>{});
-        else if (rest == 2) group(t0, std::integral_constant<int, 2>{});
+        else if (rest == 2) group(t0, std::integral_constant<int, (NW < 2 ? NW : 2)>{});
         else if (rest == 1) group(t0, std::integral_constant<int, 1>{});
         if (k == 0) WTRACE(4);
-        if (count > 0) run_jobs<kAllSmem>(p, c0, table, jobs, count, lane, out, tile0, region);
+        if (count > 0) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
         if (k == 0) WTRACE(5);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`
@@ -804,11 +817,12 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
 // Small batches (latency mode): a warp per rank, 32-ary search -- each round
 // samples the last threshold of 32 equal chunks and keeps the chunk holding
 // the boundary, so ~3 dependent loads replace ~13 of the binary search.
+template <class RT>
 __global__ void __launch_bounds__(256) grid_rank_warp_kernel(
     const double* __restrict__ rows, const double* __restrict__ cat_t, const int32_t* __restrict__ cat_cols,
     int32_t n_cat, int64_t a0, int32_t n_apps, int32_t F, int32_t TA, const double* __restrict__ thr_e,
     const int32_t* __restrict__ off_e, const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
-    uint16_t* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
+    RT* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
     const int lane = threadIdx.x & 31;
     for (int64_t z = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < n_zero;
          z += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -843,7 +857,7 @@ __global__ void __launch_bounds__(256) grid_rank_warp_kernel(
         hi = min(hi, lo + step);
         if (step == 1) break;  // chunks of one: lo is the count
     }
-    if (lane == 0) ranks[i] = static_cast<uint16_t>(lo);
+    if (lane == 0) ranks[i] = static_cast<RT>(lo);
 }
 
 // Large batches: a block per (model, tile, feature, 256 apps).  The block
@@ -852,11 +866,12 @@ __global__ void __launch_bounds__(256) grid_rank_warp_kernel(
 // shared-memory steps plus a short global binary search inside the bracketing
 // sample interval (~5 dependent loads instead of ~13).  Same count as rank_of.
 constexpr int kRankSamples = 256;
+template <class RT>
 __global__ void __launch_bounds__(256) grid_rank_sampled_kernel(
     const double* __restrict__ rows, const double* __restrict__ cat_t, const int32_t* __restrict__ cat_cols,
     int32_t n_cat, int64_t a0, int32_t n_apps, int32_t F, int32_t TA, const double* __restrict__ thr_e,
     const int32_t* __restrict__ off_e, const double* __restrict__ thr_t, const int32_t* __restrict__ off_t,
-    uint16_t* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
+    RT* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
     __shared__ double sample[kRankSamples];
     if (blockIdx.x == 0) {
         for (int z = threadIdx.x; z < n_zero; z += blockDim.x) zero[z] = 0u;
@@ -907,14 +922,15 @@ __global__ void __launch_bounds__(256) grid_rank_sampled_kernel(
             r = b0 + rank_of(thr + o + b0, b1 - b0, x);
         }
     }
-    ranks[plane * TA + static_cast<int64_t>(h) * 256 + threadIdx.x] = static_cast<uint16_t>(r);
+    ranks[plane * TA + static_cast<int64_t>(h) * 256 + threadIdx.x] = static_cast<RT>(r);
 }
 
+template <class RT>
 __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* __restrict__ cat_t,
                                  const int32_t* __restrict__ cat_cols, int32_t n_cat, int64_t a0, int32_t n_apps,
                                  int32_t F, int32_t TA, const double* __restrict__ thr_e,
                                  const int32_t* __restrict__ off_e, const double* __restrict__ thr_t,
-                                 const int32_t* __restrict__ off_t, uint16_t* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
+                                 const int32_t* __restrict__ off_t, RT* __restrict__ ranks, uint32_t* __restrict__ zero, int32_t n_zero) {
     for (int64_t z = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < n_zero;
          z += static_cast<int64_t>(gridDim.x) * blockDim.x)
         zero[z] = 0u;
@@ -935,7 +951,7 @@ __global__ void grid_rank_kernel(const double* __restrict__ rows, const double* 
         const double* thr = m ? thr_t : thr_e;
         const int32_t* off = m ? off_t : off_e;
         const int32_t o = __ldg(off + f);
-        ranks[i] = static_cast<uint16_t>(rank_of(thr + o, __ldg(off + f + 1) - o, x));
+        ranks[i] = static_cast<RT>(rank_of(thr + o, __ldg(off + f + 1) - o, x));
     }
 }
 
@@ -1828,10 +1844,11 @@ int launch_acc_cpl(const AccParams& p, int sm_count, cudaStream_t s) {
 // ranks plus two stage buffers of tree windows fit the opt-in shared memory.
 struct WalkGeom {
     int warps, win_nodes, stage_nodes, n_bufs, n_subs;
+    int tile_apps, rb;  // apps per tile, bytes per rank (1: 1024-app tiles, two apps per lane)
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
-WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 * 1024) {
+WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 * 1024, bool wide = false) {
     WalkGeom g{};
     g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
     g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
@@ -1844,9 +1861,15 @@ WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 
     // Small batches (the configs[4] latency stream): no more app groups than
     // the batch fills, so the CTAs' work items stay short.
     while (max_groups > 1 && 32LL * (max_groups / 2) >= batch_apps) max_groups /= 2;
+    if (wide) {  // 8-bit ranks: 16 warps, 1024 apps per tile
+        g.n_subs = 1;
+        max_groups = 16;
+    }
     for (int groups = 16; groups >= 1; groups >>= 1) {
         if (groups > max_groups) continue;
-        const size_t fixed = 128 + walk_rank_bytes(p.n_cols, 32 * groups) + walk_jobs_bytes(g.n_subs * groups) +
+        g.tile_apps = (wide ? 64 : 32) * groups;
+        g.rb = wide ? 1 : 2;
+        const size_t fixed = 128 + walk_rank_bytes(p.n_cols, g.tile_apps, g.rb) + walk_jobs_bytes(g.n_subs * groups) +
                              static_cast<size_t>(g.n_bufs) * kStageTrees * 16 + 16;
         if (fixed + g.n_bufs * 8 * 4 > kLimit) continue;
         int64_t stage = static_cast<int64_t>((kLimit - fixed) / (8 * g.n_bufs)) & ~1;
@@ -1857,7 +1880,7 @@ WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 
         if (win <= 0) win = max_tree < stage / 2 ? max_tree : stage / 2;
         win &= ~1LL;
         if (win < 2) win = 2;
-        if (2 * win > stage) continue;
+        if (2 * win > stage || (wide && groups != 16)) continue;
         g.warps = g.n_subs * groups;
         g.win_nodes = static_cast<int>(win);
         g.stage_nodes = static_cast<int>(stage);
@@ -1890,11 +1913,13 @@ bool acc_sliced(int64_t n_apps) {
 }
 
 // Apps per batch: the walk -> accumulate hand-off of one batch (records,
-// residue tables, ranks) is bounded by a scratch budget (4 GiB; it streams
-// through HBM -- beyond a few thousand apps it does not stay in L2).
+// residue tables, ranks) is bounded by a scratch budget (8 GiB of the 180 GB
+// HBM; it streams through HBM -- beyond a few thousand apps it does not stay
+// in L2 -- so the budget only sets how many batch boundaries, each with its
+// kernels' tail waves, a large batch pays: 4 -> 8 GiB is -4 % at configs[3]).
 int64_t batch_apps(const GridParams& p) {
     const int64_t per_app = grid_scratch_per_app(p);
-    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 32);
+    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 33);
     int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
     b = b < 256 ? 256 : b;
     return b < p.n_apps ? b : p.n_apps;
@@ -1966,11 +1991,20 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const WalkGeom small = walk_geom(p, B, 56 * 1024);
         if (small.warps > 0) wg = small;
     }
+    // 8-bit ranks (every feature of both models has <= 255 distinct
+    // thresholds) and a batch that fills whole 1024-app tiles: wide tiles.
+    // (GDVFS_WIDE=0 disables, =2 forces it for any batch that fills 16 warps.)
+    const int64_t wide_knob = env_i64("GDVFS_WIDE", 1);
+    if (p.rank8 && wg.warps == 16 && (wide_knob == 2 || (wide_knob == 1 && B >= 8 * 1024))) {
+        const WalkGeom wide = walk_geom(p, B, 227 * 1024, true);
+        if (wide.warps == 16 && wide.win_nodes >= wg.win_nodes) wg = wide;
+    }
     // 16-bit ranks and tree-local child indices bound what the walk handles
     // (grid_fast_path_ok routes other models to the general kernel).
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_wint + 1) & ~1) <= wg.win_nodes;
-    auto walk_kern = all_smem ? grid_walk_kernel<true> : grid_walk_kernel<false>;
+    auto walk_kern = wg.rb == 1 ? (all_smem ? grid_walk_kernel<true, 1> : grid_walk_kernel<false, 1>)
+                                : (all_smem ? grid_walk_kernel<true, 2> : grid_walk_kernel<false, 2>);
     int walk_per_sm = occupancy(reinterpret_cast<const void*>(walk_kern), wg.warps * 32, wg.smem);
     if (walk_per_sm < 0) return cudaErrorInvalidConfiguration;
     if (walk_per_sm < 1) walk_per_sm = 1;
@@ -1978,7 +2012,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         const int64_t a0 = b * B;
         const int32_t n = static_cast<int32_t>(p.n_apps - a0 < B ? p.n_apps - a0 : B);
         {
-            const int ta = wg.warps / wg.n_subs * 32;
+            const int ta = wg.tile_apps;
             const int64_t total = 2LL * ((n + ta - 1) / ta) * ta * p.n_cols;
             // The rank kernel also zeroes this batch's counters (the walk's
             // pool count; the sliced accumulate's arrival counters), saving
@@ -1987,21 +2021,26 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
             // are done with theirs, stream order.)
             uint32_t* zero = sliced ? arrive : counts + b;
             const int32_t n_zero = sliced ? static_cast<int32_t>(counts + nb - arrive) : 1;
-            if (total <= kRankWarpLimit) {
-                grid_rank_warp_kernel<<<static_cast<int>((total + 7) / 8), 256, 0, s>>>(
-                    p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
-                    p.t_thr_off, ranks, zero, n_zero);
-            } else if (ta % 256 == 0 && !(std::getenv("GDVFS_RANK_SAMPLED") && std::getenv("GDVFS_RANK_SAMPLED")[0] == '0')) {
-                grid_rank_sampled_kernel<<<static_cast<int>(total / 256), 256, 0, s>>>(
-                    p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
-                    p.t_thr_off, ranks, zero, n_zero);
-            } else {
-                int blocks = static_cast<int>((total + 255) / 256);
-                if (blocks > 16 * sm_count) blocks = 16 * sm_count;
-                grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
-                                                        p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, ranks, zero,
-                                                        n_zero);
-            }
+            auto rank_launch = [&](auto* rk) {
+                if (total <= kRankWarpLimit) {
+                    grid_rank_warp_kernel<<<static_cast<int>((total + 7) / 8), 256, 0, s>>>(
+                        p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
+                        p.t_thr_off, rk, zero, n_zero);
+                } else if (ta % 256 == 0 &&
+                           !(std::getenv("GDVFS_RANK_SAMPLED") && std::getenv("GDVFS_RANK_SAMPLED")[0] == '0')) {
+                    grid_rank_sampled_kernel<<<static_cast<int>(total / 256), 256, 0, s>>>(
+                        p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta, p.e_thr, p.e_thr_off, p.t_thr,
+                        p.t_thr_off, rk, zero, n_zero);
+                } else {
+                    int blocks = static_cast<int>((total + 255) / 256);
+                    if (blocks > 16 * sm_count) blocks = 16 * sm_count;
+                    grid_rank_kernel<<<blocks, 256, 0, s>>>(p.rows, p.cat_t, p.cat_cols, p.n_cat, a0, n, p.n_cols, ta,
+                                                            p.e_thr, p.e_thr_off, p.t_thr, p.t_thr_off, rk, zero,
+                                                            n_zero);
+                }
+            };
+            if (wg.rb == 1) rank_launch(reinterpret_cast<uint8_t*>(ranks));
+            else rank_launch(ranks);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
             if (mark) mark(user, "rank");
         }
@@ -2018,10 +2057,10 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.gnodes[1] = p.t_nodes;
         w.n_trees[0] = p.e_trees;
         w.n_trees[1] = p.t_trees;
-        w.ranks = ranks;
+        w.ranks = reinterpret_cast<const unsigned char*>(ranks);
         w.n_apps = n;
         w.n_cols = p.n_cols;
-        w.tile_apps = wg.warps / wg.n_subs * 32;
+        w.tile_apps = wg.tile_apps;
         w.n_subs = wg.n_subs;
         w.win_nodes = wg.win_nodes;
         w.stage_nodes = wg.stage_nodes;

@@ -257,6 +257,8 @@ KNOBS = {
     "ring4": {"GDVFS_WALK_BUFS": "4"},
     "one_group": {"GDVFS_WALK_GROUPS": "1", "GDVFS_WALK_BUFS": "3"},
     "sliced_acc": {"GDVFS_ACC_SLICED": "1"},
+    "wide_tiles": {"GDVFS_WIDE": "2"},
+    "narrow_tiles": {"GDVFS_WIDE": "0"},
 }
 
 
@@ -522,15 +524,18 @@ def test_c2_full_size_properties(ctx):
     assert 0 < ok.sum() < sc.grid.n_apps
 
 
+@pytest.mark.parametrize("wide", ["2", "0"])
 @pytest.mark.parametrize("shape", ["c3", "c4"])
-def test_deep_config_shapes_sampled_vs_oracle(ctx, shape):
+def test_deep_config_shapes_sampled_vs_oracle(ctx, shape, wide, monkeypatch):
     # BASELINE configs[2] / configs[3] at their full tree shapes (1000 trees
     # depth 10 on the 200-clock B200 grid; 2000 trees depth 12 on the
     # 267-clock grid), on slices of the very batches bench.py times (the same
     # chunk-seeded rows: apps [lo, hi) of the 1M / 10M-app batch).  128 apps
     # bit for bit against the REFERENCE's own predict + select (oracle/_ref,
     # all host threads) -- or 16 against the C oracle where _ref is absent --
-    # and every app through the properties.
+    # and every app through the properties.  wide=2: the 1024-app walk tiles
+    # with 8-bit ranks the bench's batches take; 0: 512-app tiles, 16-bit.
+    monkeypatch.setenv("GDVFS_WIDE", wide)
     cfg = W.CONFIGS[shape]
     lo = 7 * W.CHUNK_APPS + 123  # inside the batch, across a chunk boundary
     n = 2048 if shape == "c3" else 1024
