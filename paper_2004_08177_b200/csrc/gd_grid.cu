@@ -158,7 +158,11 @@ struct WalkParams {
     int32_t n_cols;
     int32_t tile_apps;         // apps per work item = 32 * groups
     int32_t splits;            // tree-pair ranges per model
-    int32_t n_items;           // tiles * 2 * splits, tile-major
+    int32_t tiles;             // app tiles in the batch
+    int32_t n_items;           // 2 * splits * tiles
+    int32_t split_major;       // item order: (model, split, tile) if set, else (tile, model, split)
+    int32_t chunk;             // consecutive items per fetch
+    uint32_t* item_next;       // chunk counter (zeroed per batch)
     int32_t win_nodes;         // per-tree window staged in shared memory (BFS prefix, even)
     int32_t stage_nodes;       // capacity of one stage buffer (walk nodes)
     int32_t n_bufs;            // stage buffers in the ring (2..4)
@@ -302,13 +306,24 @@ __device__ __forceinline__ void store_rec(TreeRec* dst, const TreeRec& r) {
     __stcs(reinterpret_cast<int4*>(dst), make_int4(static_cast<int>(r.info), r.ref, r.ref2, static_cast<int>(r.pad)));
 }
 
-// Per-CTA share of the residue-table pool: CTA b allocates from
-// [b * cap / grid, (b + 1) * cap / grid) with a shared-memory counter (no
-// global atomics; tables that do not fit become FULL records).
+// Residue-table pool: the first 3/4 are per-CTA shares -- CTA b allocates
+// from [b * R / grid, (b + 1) * R / grid) with a shared-memory counter (no
+// global atomics) -- and a CTA whose share is used up takes from the last
+// quarter through one global counter (CTAs' shares fill unevenly when the
+// work items are few, e.g. the configs[4] 64-app batches).  Tables that fit
+// in neither become FULL records.
 struct PoolRegion {
-    uint32_t* next;  // shared
+    uint32_t* next;      // shared
     uint32_t end;
+    uint32_t* ovf_next;  // global, zeroed per batch
+    uint32_t ovf_base, cap;
 };
+__device__ __forceinline__ uint32_t pool_take2(const PoolRegion& r) {
+    uint32_t idx = atomicAdd(r.next, 2u);
+    if (idx + 2u <= r.end) return idx;
+    idx = r.ovf_base + atomicAdd(r.ovf_next, 2u);
+    return idx + 2u <= r.cap ? idx : 0xffffffffu;
+}
 
 // Resolve a tree whose root walk stopped at clock node `w0` into its record,
 // one lane per job, depth-first: the clock node's children are walked
@@ -391,7 +406,7 @@ __device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCt
         }
         // A clock node at heap position P.
         const int lev = 31 - __clz(static_cast<int>(P) + 1);
-        if (lev >= GD_RES_LEVELS || (!q && (idx = atomicAdd(region.next, 2u)) + 2u > region.end)) {
+        if (lev >= GD_RES_LEVELS || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
             if (pend_dst) *pend_dst = pend_v;
             r.info = kRecFull;
             r.ref = s.groot + (w0.n >> 3);
@@ -510,13 +525,29 @@ struct ItemInfo {
     int32_t tile, model, p0, p1;
 };
 
+// Items are handed out in chunks of consecutive items by one global counter,
+// so no CTA idles while others still have work (trained ensembles' items
+// differ widely in cost).  Default order (model, split, tile), one item per
+// fetch: the CTAs in flight at any moment work on a few consecutive tree
+// ranges (megabytes: L2-resident even for models larger than L2, so each
+// range is read from HBM about once per batch, not once per tile); the
+// alternative (tile, model, split) order lets a chunk's items share their
+// tile's staged ranks.
 __device__ __forceinline__ ItemInfo item_info(const WalkParams& p, int32_t it) {
     ItemInfo r;
-    const int32_t per_tile = 2 * p.splits;
-    r.tile = it / per_tile;
-    const int32_t k = it - r.tile * per_tile;
-    r.model = k / p.splits;
-    const int32_t split = k - r.model * p.splits;
+    int32_t split;
+    if (p.split_major) {
+        const int32_t k = it / p.tiles;
+        r.tile = it - k * p.tiles;
+        r.model = k / p.splits;
+        split = k - r.model * p.splits;
+    } else {
+        const int32_t per_tile = 2 * p.splits;
+        r.tile = it / per_tile;
+        const int32_t k = it - r.tile * per_tile;
+        r.model = k / p.splits;
+        split = k - r.model * p.splits;
+    }
     const int64_t pairs = (p.n_trees[r.model] + 1) >> 1;
     r.p0 = static_cast<int32_t>(pairs * split / p.splits);
     r.p1 = static_cast<int32_t>(pairs * (split + 1) / p.splits);
@@ -567,13 +598,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // the stage is one bulk copy; otherwise each window is copied on its own.
 // Arms the buffer's barrier (or arrives on it for an invalid stage).
 template <bool kAllSmem>
-__device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& q, int lane,
+__device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int32_t& chunk_end, int32_t& q, int lane,
                            uint32_t buf_saddr, uint32_t bar, int4* table, Stage* desc) {
     while (it < it_end) {
         const ItemInfo ii = item_info(p, it);
         if (q < ii.p0) q = ii.p0;
         if (q >= ii.p1) {
-            ++it;
+            if (++it >= chunk_end) {  // next chunk
+                uint32_t nx = 0;
+                if (lane == 0) nx = atomicAdd(p.item_next, 1u);
+                it = static_cast<int32_t>(__shfl_sync(kFull, nx, 0)) * p.chunk;
+                chunk_end = min(it + p.chunk, it_end);
+            }
             q = -1;
             continue;
         }
@@ -663,23 +699,28 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     uint32_t* pool_next = reinterpret_cast<uint32_t*>(tables + NB * kStageTrees);
     PoolRegion region;
     region.next = pool_next;
-    region.end = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x + 1) * p.pool_cap / gridDim.x);
+    const uint32_t shared_cap = p.pool_cap / 4 * 3;
+    region.end = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x + 1) * shared_cap / gridDim.x);
+    region.ovf_next = p.pool_count;
+    region.ovf_base = shared_cap;
+    region.cap = p.pool_cap;
     WTRACE(0);
-    const int32_t it_begin = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x) * p.n_items / gridDim.x);
-    const int32_t it_end = static_cast<int32_t>(static_cast<int64_t>(blockIdx.x + 1) * p.n_items / gridDim.x);
+    const int32_t it_end = p.n_items;
+    int32_t* first_item = reinterpret_cast<int32_t*>(pool_next + 1);
 
     // full[b]: thread 0's arrive + the stage's TMA bytes; empty[b]: one arrive
     // per warp once done with the stage.  Warps run decoupled; thread 0
     // refills a buffer (NB - 1 stages ahead) only after every warp released it.
     const int nwarps = blockDim.x >> 5;
-    int32_t cur_it = it_begin, cur_q = -1;  // warp 0's schedule cursor
+    int32_t cur_it = 0, cur_end = 0, cur_q = -1;  // warp 0's schedule cursor (item, end of its chunk, pair)
     auto produce = [&](int j) {  // warp 0: plan stage j into buffer j % NB
         const int b = j % NB;
-        plan_stage<kAllSmem>(p, it_end, cur_it, cur_q, lane, bufs0 + static_cast<uint32_t>(b * buf_bytes), bar0 + 8 * b,
+        plan_stage<kAllSmem>(p, it_end, cur_it, cur_end, cur_q, lane, bufs0 + static_cast<uint32_t>(b * buf_bytes), bar0 + 8 * b,
                              tables + b * kStageTrees, desc + b);
     };
     if (threadIdx.x == 0) {
-        *pool_next = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * p.pool_cap / gridDim.x);
+        *pool_next = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * shared_cap / gridDim.x);
+        *first_item = static_cast<int32_t>(atomicAdd(p.item_next, 1u)) * p.chunk;
         for (int b = 0; b < NB; ++b) {
             mbar_init(bar0 + 8 * b, 1);
             mbar_init(bar0 + 32 + 8 * b, nwarps);
@@ -687,6 +728,9 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    const int32_t it_begin = *first_item;
+    cur_it = it_begin;
+    cur_end = min(it_begin + p.chunk, it_end);
     if (warp == 0) {
         for (int j = 0; j + 1 < NB; ++j) produce(j);
     }
@@ -1896,13 +1940,15 @@ int64_t env_i64(const char* name, int64_t dflt) {
     return e ? std::atoll(e) : dflt;
 }
 
-// Residue-table pool slots per app: 1/3 of the trees (a table takes two
-// slots while it is built; GDVFS_POOL_DIV overrides the divisor; tables that
-// do not fit fall back to FULL records).
+// Residue-table pool slots per app: half the trees, i.e. one table (two
+// slots: a table may grow to depth 4 in place) per four (app, tree) pairs
+// -- 12 % of the pairs hold a table at configs[3], 16 % with trained
+// configs[1] models.  GDVFS_POOL_DIV overrides the divisor; tables that do
+// not fit fall back to FULL records.
 int64_t pool_per_app(const GridParams& p) {
-    int64_t div = env_i64("GDVFS_POOL_DIV", 3);
+    int64_t div = env_i64("GDVFS_POOL_DIV", 2);
     if (div < 1) div = 1;
-    return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 1;
+    return (static_cast<int64_t>(p.e_trees) + p.t_trees) / div + 2;
 }
 
 // Latency mode for small batches: one warp pair per (app, 32-clock slice)
@@ -1946,7 +1992,7 @@ size_t grid_scratch_bytes(const GridParams& p, bool general) {
     const int64_t nb = (p.n_apps + b - 1) / b;
     // + one tile of rank padding (the rank layout is whole walk tiles)
     return static_cast<size_t>(b * grid_scratch_per_app(p)) + 4LL * kMaxTileApps * p.n_cols + 16 +
-           static_cast<size_t>(nb) * 4 + 256;
+           static_cast<size_t>(nb) * 8 + 256;
 }
 
 int launch_grid_select(const GridParams& p, bool general, int sm_count, void* stream, void* scratch,
@@ -2019,8 +2065,8 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
             // two memset launches on the latency path.
             // (Sliced: arrive[] and counts[] are adjacent; earlier batches
             // are done with theirs, stream order.)
-            uint32_t* zero = sliced ? arrive : counts + b;
-            const int32_t n_zero = sliced ? static_cast<int32_t>(counts + nb - arrive) : 1;
+            uint32_t* zero = sliced ? arrive : counts + 2 * b;
+            const int32_t n_zero = sliced ? static_cast<int32_t>(counts + 2 * nb - arrive) : 2;
             auto rank_launch = [&](auto* rk) {
                 if (total <= kRankWarpLimit) {
                     grid_rank_warp_kernel<<<static_cast<int>((total + 7) / 8), 256, 0, s>>>(
@@ -2068,16 +2114,26 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.rec[0] = rec_e;
         w.rec[1] = rec_t;
         w.pool = pool;
-        w.pool_count = counts + b;
+        w.pool_count = counts + 2 * b;
+        w.item_next = counts + 2 * b + 1;
         w.pool_cap = static_cast<uint32_t>(pool_cap);
         const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;
         const int64_t max_pairs = pe > pt ? pe : pt;
-        int64_t splits = (8LL * sm_count + 2 * tiles - 1) / (2 * tiles);
+        // Split-major items, one per fetch, ~16 per CTA (measured against
+        // tile-major chunks: configs[2] walk -12 %, trained configs[1] -40 %,
+        // configs[1] +7 %, the rank restaging per item).  GDVFS_WALK_SPLIT_MAJOR=0:
+        // tile-major, ~8 items per CTA in chunks of a quarter of that.
+        const bool split_major = env_i64("GDVFS_WALK_SPLIT_MAJOR", 1) != 0;
+        int64_t splits = ((split_major ? 16LL : 8LL) * sm_count + 2 * tiles - 1) / (2 * tiles);
         splits = env_i64("GDVFS_WALK_SPLITS", splits);
         if (splits > max_pairs) splits = max_pairs;
         if (splits < 1) splits = 1;
         w.splits = static_cast<int32_t>(splits);
+        w.tiles = static_cast<int32_t>(tiles);
         w.n_items = static_cast<int32_t>(tiles * 2 * splits);
+        w.split_major = split_major ? 1 : 0;
+        const int64_t per_cta = (w.n_items + sm_count - 1) / sm_count;
+        w.chunk = split_major ? 1 : static_cast<int32_t>(per_cta / 4 > 1 ? per_cta / 4 : 1);
         const int grid = w.n_items < sm_count * walk_per_sm ? w.n_items : sm_count * walk_per_sm;
         walk_kern<<<grid, wg.warps * 32, wg.smem, s>>>(w);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;

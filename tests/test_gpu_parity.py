@@ -259,6 +259,8 @@ KNOBS = {
     "sliced_acc": {"GDVFS_ACC_SLICED": "1"},
     "wide_tiles": {"GDVFS_WIDE": "2"},
     "narrow_tiles": {"GDVFS_WIDE": "0"},
+    "split_major": {"GDVFS_WALK_SPLIT_MAJOR": "1", "GDVFS_WALK_SPLITS": "7"},
+    "tile_major": {"GDVFS_WALK_SPLIT_MAJOR": "0", "GDVFS_WALK_SPLITS": "3"},
 }
 
 
