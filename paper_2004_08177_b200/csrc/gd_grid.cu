@@ -1959,13 +1959,14 @@ bool acc_sliced(int64_t n_apps) {
 }
 
 // Apps per batch: the walk -> accumulate hand-off of one batch (records,
-// residue tables, ranks) is bounded by a scratch budget (8 GiB of the 180 GB
+// residue tables, ranks) is bounded by a scratch budget (16 GiB of the 180 GB
 // HBM; it streams through HBM -- beyond a few thousand apps it does not stay
 // in L2 -- so the budget only sets how many batch boundaries, each with its
-// kernels' tail waves, a large batch pays: 4 -> 8 GiB is -4 % at configs[3]).
+// kernels' tail waves, a large batch pays: 4 -> 8 -> 16 GiB is -4 % / -1.5 %
+// at configs[3]).  Smaller calls allocate only what they use.
 int64_t batch_apps(const GridParams& p) {
     const int64_t per_app = grid_scratch_per_app(p);
-    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 33);
+    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 34);
     int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
     b = b < 256 ? 256 : b;
     return b < p.n_apps ? b : p.n_apps;
