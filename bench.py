@@ -557,10 +557,10 @@ def extras(args, main_arm, dev, ctx, stream, flush):
         except Exception as e:  # an extra must not cost the headline line
             out[name] = {"error": repr(e)}
     try:
-        c1 = run_c1(argparse.Namespace(apps=100, steps=5), "ours")
+        c1 = run_c1(argparse.Namespace(apps=100, steps=9), "ours")
         out["c1"] = {k: c1[k] for k in ("config", "value", "unit", "ms_per_step", "decisions_per_s", "cpu_baseline",
                                         "decisions_identical_to_reference")}
-        c1k = run_c1(argparse.Namespace(apps=1000, steps=3), "ours")
+        c1k = run_c1(argparse.Namespace(apps=1000, steps=9), "ours")
         out["c1_1000_jobs"] = {k: c1k[k] for k in ("value", "ms_per_step", "decisions_per_s", "cpu_baseline",
                                                    "decisions_identical_to_reference")}
     except Exception as e:  # noqa: BLE001

@@ -9,6 +9,6 @@ timeout 1200 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$T
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-extras --no-cpu-baseline --no-clocks --e2e-steps 1 \
     > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?" >> gpurun_out/ncu_launch_$TAG.log
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"grid_(walk|acc)" -s 10 -c 2 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"grid_(walk|acc)" -s 600 -c 2 \
     -o gpurun_out/prof_$TAG -f python bench.py --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --e2e-steps 1 \
     > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?" >> gpurun_out/ncu_full_$TAG.log

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Copy the ncu / bench evidence of one GPU run from gpurun_out/ into profiles/.
 
-    python scripts/make_profiles.py <gpurun tag> <round tag>
+    python scripts/make_profiles.py <gpurun tag> <round tag> [config]
 
 Writes profiles/<round>_launches.csv (per-kernel launch list: count, mean
 duration, DRAM bytes, share of GPU time), profiles/<round>_grid_kernel.txt
@@ -47,11 +47,18 @@ def launches(tag, rnd):
                         round(v["gpu__time_duration.sum"] / total, 4)])
 
 
+def report(tag):
+    for name in (f"prof_grid_{tag}.ncu-rep", f"prof_{tag}.ncu-rep"):
+        if (OUT / name).exists():
+            return OUT / name
+    return None
+
+
 def full_traffic(tag):
     """DRAM read+write bytes of one grid_acc_kernel launch (the dominant kernel)
     from the ncu --set full capture."""
-    rep = OUT / f"prof_grid_{tag}.ncu-rep"
-    if not rep.exists():
+    rep = report(tag)
+    if rep is None:
         return None
     out = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics",
                           "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
@@ -69,7 +76,7 @@ def full_traffic(tag):
 
 
 def kernel_summary(tag, rnd):
-    rep = OUT / f"prof_grid_{tag}.ncu-rep"
+    rep = report(tag)
     parts = []
     for cmd in (["python", "scripts/ncu_summary.py", str(rep), "--raw",
                  r"dram__bytes_(read|write)\.sum$|lts__t_bytes\.sum$|l1tex__t_sector_hit_rate\.pct$|"
@@ -86,10 +93,11 @@ def kernel_summary(tag, rnd):
 
 def main():
     tag, rnd = sys.argv[1], sys.argv[2]
+    config = sys.argv[3] if len(sys.argv) > 3 else "c4"
     PROF.mkdir(exist_ok=True)
     launches(tag, rnd)
     traffic = full_traffic(tag)
-    if (OUT / f"prof_grid_{tag}.ncu-rep").exists():
+    if report(tag) is not None:
         kernel_summary(tag, rnd)
     bench = {}
     for name in (f"bench_{tag}.json", f"bench_ref_{tag}.json"):
@@ -101,7 +109,7 @@ def main():
     if traffic is not None:
         t = PROF / "ncu_traffic.json"
         d = json.loads(t.read_text()) if t.exists() else {}
-        d["c2"] = traffic
+        d[config] = traffic
         t.write_text(json.dumps(d, indent=1))
     print("traffic", traffic)
 
