@@ -325,27 +325,61 @@ __device__ __forceinline__ uint32_t pool_take2(const PoolRegion& r) {
     return idx + 2u <= r.cap ? idx : 0xffffffffu;
 }
 
-// Resolve a tree whose root walk stopped at clock node `w0` into its record,
-// one lane per job, depth-first: the clock node's children are walked
-// row-only to their next event (leaf or clock node); a clock node at level
-// < 4 adds a test (its right child is pushed, the left one walked next), a
-// leaf is stored in its depth-4 slot.  One test between two leaves -> SM /
-// MEM (no table); tests on up to 3 levels -> TABLE (the depth-4 layout
-// compacted into one 128-byte slot); 4 levels -> TABLE4 (two slots); deeper
-// -> FULL (ref = the first clock node, per-clock traversal in the
-// accumulate kernel).  The walks between events run as an inner loop, so the
-// warp's lanes (each on its own job) handle their events together.
+__device__ __forceinline__ TreeSrc tree_src(const int4& te, bool all_smem) {
+    TreeSrc s;
+    s.wroot = te.x;
+    s.groot = te.y;
+    s.win = all_smem ? 0xffffffffu : static_cast<uint32_t>(te.z);
+    s.saddr = static_cast<uint32_t>(te.w);
+    return s;
+}
+
+// A root walk that stopped at a clock node, queued for resolution so the
+// (divergent) residue walks run with full warps.
+struct Job {
+    int32_t n;   // the clock node (byte offset within the tree)
+    int32_t t;   // tree
+    int32_t e;   // the tree's entry in the stage table (roots, window, shared address)
+    int32_t li;  // app within the tile
+};
+#ifndef GD_JOB_PAIR
+#define GD_JOB_PAIR 0
+#endif
+#ifndef GD_JOB_RUN
+#define GD_JOB_RUN 64
+#endif
+constexpr int kJobRun = GD_JOB_RUN;  // a run starts once this many are queued (and at the end of a stage)
+constexpr int kJobCap = kJobRun + 32;  // queued jobs per warp
+
+// Resolve the queued jobs, one lane per job, depth-first: the clock node's
+// children are walked row-only to their next event (leaf or clock node); a
+// clock node at level < 4 adds a test (its right child is pushed, the left
+// one walked next), a leaf is stored in its depth-4 slot.  One test between
+// two leaves -> SM / MEM (no table); tests on up to 3 levels -> TABLE (the
+// depth-4 layout compacted into one 128-byte slot); 4 levels -> TABLE4 (two
+// slots); deeper -> FULL (ref = the first clock node, per-clock traversal in
+// the accumulate kernel).  The walks between events run as an inner loop, so
+// the warp's lanes (each on its own job) handle their events together, and
+// a lane that finishes its job takes the next queued one at once: the run
+// costs about the longest lane's SUM of jobs, not the sum over rounds of the
+// longest job of each round of 32.  Out of line: reached from every
+// walk-group width and the drain, one copy keeps the kernel in the I-cache.
 template <bool kAllSmem, int RB>
-__device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCtx& c, const TreeSrc& s, const Walk& w0,
-                                               const PoolRegion& region) {
-    TreeRec r{0u, 0, 0, 0u};
-    const uint2 t0 = test_mk(w0);
+__device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
+                                      int& count, int lane, TreeRec* out, int64_t tile0, const PoolRegion& region) {
+    const int n_jobs = count;
+    const unsigned lt = (1u << lane) - 1u;
+    int next = min(32, n_jobs);  // jobs handed out (warp-uniform)
+    int k = lane;
+    bool has = k < n_jobs;
+    WalkCtx c = c0;
+    TreeSrc s{0, 0, 0u, 0u};
+    Job jb{0, 0, 0, 0};
+    Walk w0{0, 0, 0}, cur{0, 0, 0};
+    uint2 t0 = make_uint2(0u, 0u);
     // Pending right children, a stack of at most 4: (byte offset << 8) | leaf << 7 | heap position.
-    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0;
-    int nst = 1;
-    st0 = (static_cast<uint32_t>(wchild(w0.fc) + 8) << 8) | (static_cast<uint32_t>((w0.fc >> 1) & 1) << 7) | 2u;
-    Walk cur = child_walk<kAllSmem>(c, s, w0, 0);
-    uint32_t P = 1;
+    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0, P = 1;
+    int nst = 0;
     // The table is built in the 128-byte RTRec form and moved to the
     // two-slot RTRec4 form only when a fourth test level appears (rare).
     RTRec4* q = nullptr;
@@ -363,131 +397,149 @@ __device__ __forceinline__ TreeRec resolve_dfs(const WalkParams& p, const WalkCt
         pend_dst = big ? &q->leaf[path << (4u - lev)] : &reinterpret_cast<RTRec*>(q)->leaf[path << (3u - lev)];
         pend_v = __ldg(&c.gnodes[leaf_idx].v);
     };
-    while (true) {
-        while (cur.fc >= 0) {  // row-only steps to the next event
-            const int32_t x = rank_value<RB>(c, cur.fc);
-            const int right = x <= cur.key ? 0 : 1;
-            const int32_t nn = wchild(cur.fc) + 8 * right;
-            if ((cur.fc >> right) & 1) {
-                cur = Walk{nn, s.groot + (nn >> 3), kLeafFc};
-            } else {
-                cur.n = nn;
-                load_wnode<kAllSmem>(c, s, cur);
-            }
+    auto start = [&]() {  // job k: its clock node, then the left child's walk
+        jb = jobs[k];
+        c.row_saddr = c0.row_saddr + static_cast<uint32_t>(jb.li * RB);
+        s = tree_src(table[jb.e], kAllSmem);
+        w0 = Walk{jb.n, 0, 0};
+        load_wnode<kAllSmem>(c, s, w0);
+        t0 = test_mk(w0);
+#if GD_JOB_PAIR
+        // Both children walked side by side to their next events: the right
+        // one's walk is pushed standing on its event.
+        Walk ab[2] = {child_walk<kAllSmem>(c, s, w0, 0), child_walk<kAllSmem>(c, s, w0, 1)};
+        {
+            const uint32_t ra[2] = {c.row_saddr, c.row_saddr};
+            const TreeSrc ss[2] = {s, s};
+            const bool vv[2] = {true, true};
+            walkn<kAllSmem, RB, 2>(c, ra, ss, vv, ab);
         }
-        if (wfeat(cur.fc) == kFeatLeaf) {
-            if (!q) {
-                if (P == 1u) {
-                    lleaf = cur.key;
-                } else {  // P == 2 with no table: one test between two leaves
-                    r.info = (wfeat(w0.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w0.key) << 16);
-                    r.ref = lleaf;
-                    r.ref2 = cur.key;
-                    return r;
+        st0 = (static_cast<uint32_t>(ab[1].n) << 8) | (wfeat(ab[1].fc) == kFeatLeaf ? 1u << 7 : 0u) | 2u;
+        cur = ab[0];
+#else
+        st0 = (static_cast<uint32_t>(wchild(w0.fc) + 8) << 8) | (static_cast<uint32_t>((w0.fc >> 1) & 1) << 7) | 2u;
+        cur = child_walk<kAllSmem>(c, s, w0, 0);
+#endif
+        nst = 1;
+        P = 1u;
+        q = nullptr;
+        big = false;
+        tmask = 1u;
+        maxlev = 0;
+        lleaf = -1;
+    };
+    if (has) start();
+    while (__any_sync(kFull, has)) {
+        bool fin = false;
+        TreeRec r{0u, 0, 0, 0u};
+        if (has) {
+            while (cur.fc >= 0) {  // row-only steps to the next event
+                const int32_t x = rank_value<RB>(c, cur.fc);
+                const int right = x <= cur.key ? 0 : 1;
+                const int32_t nn = wchild(cur.fc) + 8 * right;
+                if ((cur.fc >> right) & 1) {
+                    cur = Walk{nn, s.groot + (nn >> 3), kLeafFc};
+                } else {
+                    cur.n = nn;
+                    load_wnode<kAllSmem>(c, s, cur);
                 }
-            } else {
-                put_leaf(P, cur.key);
             }
-            if (nst == 0) break;
-            const uint32_t e = st0;
-            st0 = st1;
-            st1 = st2;
-            st2 = st3;
-            --nst;
-            P = e & 127u;
-            const int32_t n = static_cast<int32_t>(e >> 8);
-            if ((e >> 7) & 1u) {
-                cur = Walk{n, s.groot + (n >> 3), kLeafFc};
-            } else {
-                cur = Walk{n, 0, 0};
-                load_wnode<kAllSmem>(c, s, cur);
+            if (wfeat(cur.fc) == kFeatLeaf) {
+                if (!q) {
+                    if (P == 1u) {
+                        lleaf = cur.key;
+                    } else {  // P == 2 with no table: one test between two leaves
+                        r.info = (wfeat(w0.fc) == kFeatMem ? kRecMem : kRecSm) | (static_cast<uint32_t>(w0.key) << 16);
+                        r.ref = lleaf;
+                        r.ref2 = cur.key;
+                        fin = true;
+                    }
+                } else {
+                    put_leaf(P, cur.key);
+                }
+                if (!fin) {
+                    if (nst == 0) {  // the residue is complete: its table
+                        const uint32_t D = static_cast<uint32_t>(maxlev) + 1u;  // 2, 3 or 4
+                        // Leaves above the last level sit under always-left tests.
+#pragma unroll
+                        for (uint32_t z = 1; z < 15; ++z) {
+                            if (z + 1u < (1u << D) && !((tmask >> z) & 1u)) q->test[z] = make_uint2(0u, 0u);
+                            if (z == 6 && D < 4) break;
+                        }
+                        r.ref = static_cast<int32_t>(idx);
+                        if (big) {
+                            r.info = kRecTable4;
+                        } else {
+                            reinterpret_cast<RTRec*>(q)->depth = D;
+                            r.info = kRecTable;
+                        }
+                        fin = true;
+                    } else {
+                        const uint32_t e = st0;
+                        st0 = st1;
+                        st1 = st2;
+                        st2 = st3;
+                        --nst;
+                        P = e & 127u;
+                        const int32_t n = static_cast<int32_t>(e >> 8);
+                        if ((e >> 7) & 1u) {
+                            cur = Walk{n, s.groot + (n >> 3), kLeafFc};
+                        } else {
+                            cur = Walk{n, 0, 0};
+                            load_wnode<kAllSmem>(c, s, cur);
+                        }
+                    }
+                }
+            } else {  // a clock node at heap position P
+                const int lev = 31 - __clz(static_cast<int>(P) + 1);
+                if (lev >= GD_RES_LEVELS || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
+                    r.info = kRecFull;
+                    r.ref = s.groot + (w0.n >> 3);
+                    fin = true;
+                } else {
+                    if (!q) {
+                        q = reinterpret_cast<RTRec4*>(p.pool + idx);
+                        q->test[0] = t0;
+                        if (lleaf >= 0) put_leaf(1u, lleaf);
+                    }
+                    if (lev == 3 && !big) {  // fourth level: depth-3 leaf slot k becomes depth-4 slot 2k
+                        if (pend_dst) *pend_dst = pend_v;
+                        pend_dst = nullptr;
+                        RTRec* t = reinterpret_cast<RTRec*>(q);
+                        double lv[8];
+#pragma unroll
+                        for (int z = 0; z < 8; ++z) lv[z] = t->leaf[z];
+#pragma unroll
+                        for (int z = 0; z < 8; ++z) q->leaf[2 * z] = lv[z];
+                        big = true;
+                    }
+                    q->test[P] = test_mk(cur);
+                    tmask |= 1u << P;
+                    maxlev = max(maxlev, lev);
+                    st3 = st2;
+                    st2 = st1;
+                    st1 = st0;
+                    st0 = (static_cast<uint32_t>(wchild(cur.fc) + 8) << 8) |
+                          (static_cast<uint32_t>((cur.fc >> 1) & 1) << 7) | (2u * P + 2u);
+                    ++nst;
+                    cur = child_walk<kAllSmem>(c, s, cur, 0);
+                    P = 2u * P + 1u;
+                }
             }
-            continue;
+            if (fin) store_rec(out + rec_index(jb.t, tile0 + jb.li, p.n_apps), r);
         }
-        // A clock node at heap position P.
-        const int lev = 31 - __clz(static_cast<int>(P) + 1);
-        if (lev >= GD_RES_LEVELS || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
-            if (pend_dst) *pend_dst = pend_v;
-            r.info = kRecFull;
-            r.ref = s.groot + (w0.n >> 3);
-            return r;
+        // Lanes that finished a job take the next queued ones.
+        const unsigned fm = __ballot_sync(kFull, fin);
+        if (fm) {
+            if (fin) {
+                k = next + __popc(fm & lt);
+                has = k < n_jobs;
+                if (has) start();
+            }
+            next += __popc(fm);
         }
-        if (!q) {
-            q = reinterpret_cast<RTRec4*>(p.pool + idx);
-            q->test[0] = t0;
-            if (lleaf >= 0) put_leaf(1u, lleaf);
-        }
-        if (lev == 3 && !big) {  // fourth level: depth-3 leaf slot k becomes depth-4 slot 2k
-            if (pend_dst) *pend_dst = pend_v;
-            pend_dst = nullptr;
-            RTRec* t = reinterpret_cast<RTRec*>(q);
-            double lv[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) lv[k] = t->leaf[k];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) q->leaf[2 * k] = lv[k];
-            big = true;
-        }
-        q->test[P] = test_mk(cur);
-        tmask |= 1u << P;
-        maxlev = max(maxlev, lev);
-        st3 = st2;
-        st2 = st1;
-        st1 = st0;
-        st0 = (static_cast<uint32_t>(wchild(cur.fc) + 8) << 8) | (static_cast<uint32_t>((cur.fc >> 1) & 1) << 7) |
-              (2u * P + 2u);
-        ++nst;
-        cur = child_walk<kAllSmem>(c, s, cur, 0);
-        P = 2u * P + 1u;
     }
     if (pend_dst) *pend_dst = pend_v;
-    const uint32_t D = static_cast<uint32_t>(maxlev) + 1u;  // 2, 3 or 4
-    // Leaves above the last level sit under always-left tests.
-#pragma unroll
-    for (uint32_t k = 1; k < 15; ++k) {
-        if (k + 1u < (1u << D) && !((tmask >> k) & 1u)) q->test[k] = make_uint2(0u, 0u);
-        if (k == 6 && D < 4) break;
-    }
-    r.ref = static_cast<int32_t>(idx);
-    if (big) {
-        r.info = kRecTable4;
-        return r;
-    }
-    reinterpret_cast<RTRec*>(q)->depth = D;
-    r.info = kRecTable;
-    return r;
-}
-
-// A root walk that stopped at a clock node, queued for resolution so the
-// (divergent) residue walks run with full warps.
-struct Job {
-    int32_t n;   // the clock node (byte offset within the tree)
-    int32_t t;   // tree
-    int32_t e;   // the tree's entry in the stage table (roots, window, shared address)
-    int32_t li;  // app within the tile
-};
-constexpr int kJobCap = 64;
-
-// Every queued job is resolved (lane l takes jobs l, l + 32), then the queue
-// is empty.  Out of line: it is reached from every walk-group width and the
-// drain, and one copy of the residue code keeps the kernel in the I-cache.
-template <bool kAllSmem, int RB>
-__device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, const int4* table, Job* jobs,
-                                         int& count, int lane, TreeRec* out, int64_t tile0, const PoolRegion& region) {
-    for (int k = lane; k < count; k += 32) {
-        const Job j = jobs[k];
-        WalkCtx c = c0;
-        c.row_saddr = c0.row_saddr + static_cast<uint32_t>(j.li * RB);
-        const int4 te = table[j.e];  // shared: no global round trip before the residue walk
-        TreeSrc s;
-        s.wroot = te.x;
-        s.groot = te.y;
-        s.win = kAllSmem ? 0xffffffffu : static_cast<uint32_t>(te.z);
-        s.saddr = static_cast<uint32_t>(te.w);
-        Walk w{j.n, 0, 0};
-        load_wnode<kAllSmem>(c, s, w);
-        store_rec(out + rec_index(j.t, tile0 + j.li, p.n_apps), resolve_dfs<kAllSmem, RB>(p, c, s, w, region));
-    }
     __syncwarp();
     count = 0;
 }
@@ -504,7 +556,7 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, e, li};
     count += __popc(m);
     __syncwarp();
-    if (count >= 32) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
+    if (count >= kJobRun) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
 }
 
 constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
