@@ -398,8 +398,17 @@ bool takes_fast_path(const gd_model* me, const gd_model* mt, const gd_grid& g, c
 // (the host-buffer path marks its copies around the kernels).  Catalogs wider
 // than gd::kMaxClocks run in 512-clock chunks that write the E/T tables
 // (row stride = the full catalog), then one wide selection.
+// Host-side inputs of a large host-buffer call, streamed batch by batch
+// (grid_select_host).
+struct StreamedInputs {
+    const double* rows;
+    const double* cat_t;
+    const double* budgets;
+};
+
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
-              gd_decision* d_out, double* d_e, double* d_t, bool begin_timing = true, bool force_general = false) {
+              gd_decision* d_out, double* d_e, double* d_t, bool begin_timing = true, bool force_general = false,
+              const StreamedInputs* sin = nullptr) {
     if (g.n_apps == 0) return GD_OK;
     const bool general = !takes_fast_path(me, mt, g, o, force_general);
     if (!general) {
@@ -413,6 +422,26 @@ int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid
     p.t_out = d_t;
     const int64_t A = g.n_apps, C = g.n_clocks;
     const bool wide = C > gd::kMaxClocks;
+    if (sin) {  // the caller left rows / cat_t / budgets on the host for this path
+        if (general || wide) return set_error(GD_ERR_UNSUPPORTED, "grid_impl: streamed inputs on a chunked path");
+        const int64_t B = gd::grid_batch_apps(p), nb = (A + B - 1) / B;
+        if (!ctx->copy_stream) GD_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "copy stream");
+        while (static_cast<int64_t>(ctx->batch_events.size()) < nb + 1) {
+            cudaEvent_t ev;
+            GD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "batch event");
+            ctx->batch_events.push_back(ev);
+        }
+        // The copy stream starts after everything already on the call's stream
+        // (the scratch allocation and the other inputs).
+        cudaEvent_t start = ctx->batch_events[nb];
+        GD_CUDA(cudaEventRecord(start, ctx->stream), "copy start event");
+        GD_CUDA(cudaStreamWaitEvent(ctx->copy_stream, start, 0), "copy stream wait");
+        p.h_rows = sin->rows;
+        p.h_cat_t = sin->cat_t;
+        p.h_budgets = sin->budgets;
+        p.copy_stream = ctx->copy_stream;
+        p.batch_ready = reinterpret_cast<void* const*>(ctx->batch_events.data());
+    }
     // General mode reads per-record time rows (the categorical columns
     // replaced by their time encoding); wide mode needs the full tables.
     Scratch side{ctx->stream};
@@ -532,6 +561,11 @@ int gd_ctx_destroy(gd_ctx* ctx) {
     if (ctx->stage) cudaFreeHost(ctx->stage);
     for (gd_graph_entry& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
     if (ctx->out_stage) cudaFreeHost(ctx->out_stage);
+    if (ctx->copy_stream) {
+        cudaStreamSynchronize(ctx->copy_stream);
+        cudaStreamDestroy(ctx->copy_stream);
+    }
+    for (cudaEvent_t ev : ctx->batch_events) cudaEventDestroy(ev);
     for (gd_pbuf& b : ctx->pbuf) {
         if (b.ev) cudaEventDestroy(b.ev);
         if (b.base) cudaFree(b.base);
@@ -1013,6 +1047,15 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     }
     GD_CUDA(s.alloc(), "cudaMallocAsync");
     if (ctx->timing) timing_begin(ctx);
+    // A large call of several app batches on the fast path streams its rows
+    // in batch by batch, overlapping the upload with the kernels
+    // (GDVFS_STREAM_INPUTS=0 disables).
+    bool stream_in = false;
+    if (in_end0 > kStageLimit && !g->rec_of_clock && C <= gd::kMaxClocks && !force_general &&
+        takes_fast_path(me, mt, *g, *o, force_general)) {
+        const char* env = std::getenv("GDVFS_STREAM_INPUTS");
+        if (!env || env[0] != '0') stream_in = gd::grid_batch_apps(grid_params(me, mt, *g, *o, false)) < A;
+    }
     // Inputs occupy the scratch prefix [0, in_end).  Small calls (the online
     // stream's 64-job batches) pack them into pinned staging with the same
     // offsets and move them in ONE copy: per-copy latency, not bandwidth,
@@ -1031,6 +1074,17 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
         }
         GD_CUDA(cudaMemcpyAsync(s.base, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream), "H2D staged inputs");
         GD_CUDA(cudaEventRecord(ctx->stage_ev, ctx->stream), "stage event record");
+    } else if (stream_in) {
+        // Several app batches on the fast path: the small inputs now, rows /
+        // cat_t / budgets batch by batch on the copy stream (grid_impl).
+        for (size_t i : {i_catc, i_sm, i_mem}) {
+            const void* src = i == i_catc ? static_cast<const void*>(g->cat_cols)
+                                          : (i == i_sm ? static_cast<const void*>(g->sm_clock) : g->mem_clock);
+            if (s.pieces[i].second) {
+                GD_CUDA(cudaMemcpyAsync(s.ptr(i), src, s.pieces[i].second, cudaMemcpyHostToDevice, ctx->stream),
+                        "H2D grid input");
+            }
+        }
     } else {
         // The rows go straight from the caller's buffer; the rest (scratch
         // range [cat_t, budgets]) is packed into the pinned staging while
@@ -1074,8 +1128,9 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     dg.mem_clock = static_cast<int32_t*>(s.ptr(i_mem));
     dg.budgets = static_cast<double*>(s.ptr(i_bud));
     if (ctx->timing) timing_mark(ctx, "h2d");
+    const StreamedInputs sin{g->rows, g->cat_t, g->budgets};
     rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
-                   static_cast<double*>(s.ptr(i_t)), false, force_general);
+                   static_cast<double*>(s.ptr(i_t)), false, force_general, stream_in ? &sin : nullptr);
     if (rc) return rc;
     if (keep_dev_out) {
         *keep_dev_out = static_cast<gd_decision*>(s.ptr(i_out));

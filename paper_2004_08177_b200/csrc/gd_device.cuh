@@ -85,6 +85,15 @@ struct GridParams {
     int32_t n_cols, n_cat, n_clocks, sm_col, mem_col;
     int32_t mode, objective, best_effort;
     int64_t out_stride;  // row stride of e_out / t_out (n_clocks, or the full catalog for a clock chunk)
+    // Host-buffer calls of several app batches (launch_grid_select, fast
+    // path, rec_of_clock null): rows / cat_t / budgets still on the host
+    // (pinned); batch b's slices are copied on `copy_stream` and batch b's
+    // kernels wait for `batch_ready[b]`, so the upload overlaps the compute.
+    const double* h_rows = nullptr;
+    const double* h_cat_t = nullptr;
+    const double* h_budgets = nullptr;
+    void* copy_stream = nullptr;
+    void* const* batch_ready = nullptr;  // cudaEvent_t[n_batches]
 };
 
 struct SelectParams {
@@ -112,6 +121,7 @@ int launch_build_rows_t(const double* rows, const double* cat_t, const int32_t* 
 // least grid_scratch_bytes) for the per-(app, tree) records; `launches` is
 // incremented per kernel launched.
 int64_t grid_scratch_per_app(const GridParams& p);
+int64_t grid_batch_apps(const GridParams& p);  // apps per batch of the fast path
 size_t grid_scratch_bytes(const GridParams& p, bool general);
 // `mark(name)`, if set, is called after each kernel launch (timing hook).
 typedef void (*LaunchMark)(void* user, const char* name);

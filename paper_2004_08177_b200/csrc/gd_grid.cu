@@ -2026,6 +2026,8 @@ int64_t batch_apps(const GridParams& p) {
 
 }  // namespace
 
+int64_t grid_batch_apps(const GridParams& p) { return batch_apps(p); }
+
 bool grid_fast_path_ok(const GridParams& p) {
     return p.rank16 && p.max_tree_nodes <= 65536 && walk_geom(p, batch_apps(p)).warps > 0;
 }
@@ -2107,9 +2109,33 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     int walk_per_sm = occupancy(reinterpret_cast<const void*>(walk_kern), wg.warps * 32, wg.smem);
     if (walk_per_sm < 0) return cudaErrorInvalidConfiguration;
     if (walk_per_sm < 1) walk_per_sm = 1;
+    // Streamed inputs: batch b's slices go up on the copy stream, issued after
+    // batch b - 1's kernels were enqueued (from pageable memory the copy call
+    // blocks the host, so the kernels already queued keep the GPU busy).
+    auto upload = [&](int64_t b) -> cudaError_t {
+        cudaStream_t cs = static_cast<cudaStream_t>(p.copy_stream);
+        const int64_t a0 = b * B, n = p.n_apps - a0 < B ? p.n_apps - a0 : B;
+        cudaError_t r;
+        if ((r = cudaMemcpyAsync(const_cast<double*>(p.rows) + a0 * p.n_cols, p.h_rows + a0 * p.n_cols,
+                                 static_cast<size_t>(n * p.n_cols) * sizeof(double), cudaMemcpyHostToDevice, cs)) !=
+            cudaSuccess)
+            return r;
+        if (p.n_cat > 0 &&
+            (r = cudaMemcpyAsync(const_cast<double*>(p.cat_t) + a0 * p.n_cat, p.h_cat_t + a0 * p.n_cat,
+                                 static_cast<size_t>(n * p.n_cat) * sizeof(double), cudaMemcpyHostToDevice, cs)) !=
+                cudaSuccess)
+            return r;
+        if ((r = cudaMemcpyAsync(const_cast<double*>(p.budgets) + a0, p.h_budgets + a0,
+                                 static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice, cs)) != cudaSuccess)
+            return r;
+        return cudaEventRecord(static_cast<cudaEvent_t>(p.batch_ready[b]), cs);
+    };
+    if (p.h_rows && (e = upload(0)) != cudaSuccess) return e;
     for (int64_t b = 0; b < nb; ++b) {
         const int64_t a0 = b * B;
         const int32_t n = static_cast<int32_t>(p.n_apps - a0 < B ? p.n_apps - a0 : B);
+        if (p.h_rows && (e = cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(p.batch_ready[b]), 0)) != cudaSuccess)
+            return e;
         {
             const int ta = wg.tile_apps;
             const int64_t total = 2LL * ((n + ta - 1) / ta) * ta * p.n_cols;
@@ -2231,6 +2257,7 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         }
         if (mark) mark(user, "acc");
         if (launches) *launches += 3;
+        if (p.h_rows && b + 1 < nb && (e = upload(b + 1)) != cudaSuccess) return e;
     }
     return cudaSuccess;
 }

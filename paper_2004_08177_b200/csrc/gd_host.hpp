@@ -52,6 +52,10 @@ struct gd_ctx {
     gd_pbuf pbuf[2];  // 0: grid kernel scratch, 1: host-buffer call inputs / outputs
     char* out_stage = nullptr;  // pinned, kStageLimit bytes: decisions of graph replays
     std::vector<gd_graph_entry> graphs;  // most recent last
+    // Large host-buffer calls: batch inputs streamed on copy_stream, one
+    // event per batch (grow-only pool).
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> batch_events;
 };
 
 struct gd_model {

@@ -664,3 +664,22 @@ def test_many_thresholds_and_huge_trees_take_general_kernel(ctx):
     big = W.make_scenario("big", 12, "p100", 2, 16, seed=3, w_clk=0.05)
     assert big.energy.n_nodes // 2 > 65536
     _check_vs_oracle(ctx, big, combos=((0, 0, 0),))
+
+
+@pytest.mark.parametrize("stream", ["1", "0"])
+def test_streamed_batch_inputs_vs_oracle(ctx, stream, monkeypatch):
+    # A large host-buffer call of many app batches: rows / cat_t / budgets
+    # are uploaded batch by batch on the copy stream while earlier batches
+    # compute (GDVFS_STREAM_INPUTS=1), or in one upload first (0).
+    monkeypatch.setenv("GDVFS_STREAM_INPUTS", stream)
+    monkeypatch.setenv("GDVFS_BATCH_BYTES", "4000000")
+    sc = W.make_scenario("streamed", 6000, "gtx980", 60, 8, seed=31, w_clk=0.08)
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
+    budgets = W.deadlines_from_times(t0, seed=4)
+    want, we, wt = O.oracle_grid(sc.energy, sc.time, sc.grid, budgets)
+    got = gd.grid_select(me, mt, sc.grid, budgets)
+    assert decisions_equal(got, want)
+    got2, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
+    assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+    assert decisions_equal(got2, want)
