@@ -286,8 +286,10 @@ int validate_grid(const gd_model* me, const gd_model* mt, const gd_grid* g, cons
 // The partial-evaluation kernel walks a copy of the packed nodes whose clock
 // columns are recoded (gd_device.cuh kFeatSm / kFeatMem); built once per
 // (model, sm_col, mem_col) on the context stream.
-int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t mem_col) {
-    if (m->d_grid_nodes && m->grid_sm_col == sm_col && m->grid_mem_col == mem_col) return GD_OK;
+int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t mem_col, int32_t sm_fix, int32_t mem_fix) {
+    if (m->d_grid_nodes && m->grid_sm_col == sm_col && m->grid_mem_col == mem_col && m->grid_sm_fix == sm_fix &&
+        m->grid_mem_fix == mem_fix)
+        return GD_OK;
     if (m->packed_nodes == 0) return GD_OK;
     if (!m->d_grid_nodes) {
         GD_CUDA(cudaMalloc(&m->d_grid_nodes, static_cast<size_t>(m->packed_nodes) * sizeof(gd::PNode)),
@@ -303,11 +305,13 @@ int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t me
     GD_CUDA(cudaMemsetAsync(m->d_wnodes, 0, static_cast<size_t>(m->n_wnodes) * sizeof(gd::WNode), ctx->stream),
             "memset(walk nodes)");
     e = gd::launch_build_walk_nodes(m->d_grid_nodes, m->packed_nodes, m->d_roots, m->n_trees(), m->d_wroots,
-                                    m->d_thr, m->d_thr_off, m->d_wnodes, ctx->stream);
+                                    m->d_thr, m->d_thr_off, sm_fix, mem_fix, m->d_wnodes, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "walk-node kernel");
     m->grid_sm_col = sm_col;
     m->grid_mem_col = mem_col;
+    m->grid_sm_fix = sm_fix;
+    m->grid_mem_fix = mem_fix;
     return GD_OK;
 }
 
@@ -398,6 +402,22 @@ bool takes_fast_path(const gd_model* me, const gd_model* mt, const gd_grid& g, c
 // (the host-buffer path marks its copies around the kernels).  Catalogs wider
 // than gd::kMaxClocks run in 512-clock chunks that write the E/T tables
 // (row stride = the full catalog), then one wide selection.
+// Clock columns with ONE value across a call's catalog (a single memory
+// clock, as on the B200 / P100 grids): their tests are folded into the walk
+// nodes (launch_build_walk_nodes), so no residue carries them.  0 = varies.
+// GDVFS_FOLD=0 disables.
+void clock_fix(const int32_t* sm, const int32_t* mem, int64_t C, int32_t& sm_fix, int32_t& mem_fix) {
+    sm_fix = mem_fix = 0;
+    const char* env = std::getenv("GDVFS_FOLD");
+    if ((env && env[0] == '0') || C <= 0) return;
+    sm_fix = sm[0];
+    mem_fix = mem[0];
+    for (int64_t c = 1; c < C; ++c) {
+        if (sm[c] != sm_fix) sm_fix = 0;
+        if (mem[c] != mem_fix) mem_fix = 0;
+    }
+}
+
 // Host-side inputs of a large host-buffer call, streamed batch by batch
 // (grid_select_host).
 struct StreamedInputs {
@@ -406,14 +426,31 @@ struct StreamedInputs {
     const double* budgets;
 };
 
+// h_fix: the catalog's folded clocks (clock_fix) when the caller has the
+// catalog on the host; null reads it back from the device (not under capture).
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
               gd_decision* d_out, double* d_e, double* d_t, bool begin_timing = true, bool force_general = false,
-              const StreamedInputs* sin = nullptr) {
+              const StreamedInputs* sin = nullptr, const int32_t* h_fix = nullptr) {
     if (g.n_apps == 0) return GD_OK;
     const bool general = !takes_fast_path(me, mt, g, o, force_general);
     if (!general) {
-        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col);
-        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col);
+        int32_t fix[2] = {0, 0};
+        if (h_fix) {
+            fix[0] = h_fix[0];
+            fix[1] = h_fix[1];
+        } else {
+            std::vector<int32_t> cat(2 * static_cast<size_t>(g.n_clocks));
+            GD_CUDA(cudaMemcpyAsync(cat.data(), g.sm_clock, g.n_clocks * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    ctx->stream),
+                    "D2H catalog");
+            GD_CUDA(cudaMemcpyAsync(cat.data() + g.n_clocks, g.mem_clock, g.n_clocks * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, ctx->stream),
+                    "D2H catalog");
+            GD_CUDA(cudaStreamSynchronize(ctx->stream), "catalog sync");
+            clock_fix(cat.data(), cat.data() + g.n_clocks, g.n_clocks, fix[0], fix[1]);
+        }
+        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col, fix[0], fix[1]);
+        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col, fix[0], fix[1]);
         if (rc) return rc;
     }
     gd::GridParams p = grid_params(me, mt, g, o, general);
@@ -904,7 +941,7 @@ gd_graph_entry* find_graph(gd_ctx* ctx, const gd_graph_entry& key) {
 // every model structure built): staged inputs -> kernels -> decisions into
 // ctx->out_stage.  Failures leave no entry (the normal path keeps working).
 void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& dg, const gd_select_opts& o,
-                   gd_graph_entry key, void* dev_in, size_t in_end, gd_decision* dev_out) {
+                   gd_graph_entry key, void* dev_in, size_t in_end, gd_decision* dev_out, const int32_t* fix) {
     const size_t out_bytes = static_cast<size_t>(dg.n_apps) * sizeof(gd_decision);
     if (!ctx->out_stage && cudaHostAlloc(reinterpret_cast<void**>(&ctx->out_stage), kStageLimit, cudaHostAllocMapped) !=
                                cudaSuccess) {
@@ -927,7 +964,8 @@ void capture_graph(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd
     bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
         ok = cudaMemcpyAsync(dev_in, ctx->stage, in_end, cudaMemcpyHostToDevice, ctx->stream) == cudaSuccess;
-        ok = ok && grid_impl(ctx, me, mt, dg, o, host_out ? host_out : dev_out, nullptr, nullptr, false) == GD_OK;
+        ok = ok && grid_impl(ctx, me, mt, dg, o, host_out ? host_out : dev_out, nullptr, nullptr, false, false, nullptr,
+                             fix) == GD_OK;
         if (!host_out) {
             ok = ok &&
                  cudaMemcpyAsync(ctx->out_stage, dev_out, out_bytes, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
@@ -989,6 +1027,8 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
             }
         }
     }
+    int32_t fix[2];
+    clock_fix(g->sm_clock, g->mem_clock, C, fix[0], fix[1]);
     Scratch s{ctx->stream, &ctx->pbuf[1]};
     const size_t i_rows = s.add(static_cast<size_t>(R) * g->n_cols * sizeof(double));
     const size_t i_cat = s.add(static_cast<size_t>(R) * g->n_cat * sizeof(double));
@@ -1027,7 +1067,8 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
         // The graph holds the models' grid nodes as recoded for its clock
         // columns; a call with other columns in between rebuilt them in place.
         if (hit && (me->grid_sm_col != g->sm_col || me->grid_mem_col != g->mem_col || mt->grid_sm_col != g->sm_col ||
-                    mt->grid_mem_col != g->mem_col)) {
+                    mt->grid_mem_col != g->mem_col || me->grid_sm_fix != fix[0] || me->grid_mem_fix != fix[1] ||
+                    mt->grid_sm_fix != fix[0] || mt->grid_mem_fix != fix[1])) {
             cudaGraphExecDestroy(hit->exec);
             ctx->graphs.erase(ctx->graphs.begin() + (hit - ctx->graphs.data()));
             hit = nullptr;
@@ -1130,7 +1171,7 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     if (ctx->timing) timing_mark(ctx, "h2d");
     const StreamedInputs sin{g->rows, g->cat_t, g->budgets};
     rc = grid_impl(ctx, me, mt, dg, *o, static_cast<gd_decision*>(s.ptr(i_out)), static_cast<double*>(s.ptr(i_e)),
-                   static_cast<double*>(s.ptr(i_t)), false, force_general, stream_in ? &sin : nullptr);
+                   static_cast<double*>(s.ptr(i_t)), false, force_general, stream_in ? &sin : nullptr, fix);
     if (rc) return rc;
     if (keep_dev_out) {
         *keep_dev_out = static_cast<gd_decision*>(s.ptr(i_out));
@@ -1151,7 +1192,7 @@ int grid_select_host(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const 
     }
     if (ctx->timing) timing_mark(ctx, "d2h");
     GD_CUDA(cudaStreamSynchronize(ctx->stream), "grid sync");
-    if (graphable && ctx->stage) capture_graph(ctx, me, mt, dg, *o, key, s.base, in_end, static_cast<gd_decision*>(s.ptr(i_out)));
+    if (graphable && ctx->stage) capture_graph(ctx, me, mt, dg, *o, key, s.base, in_end, static_cast<gd_decision*>(s.ptr(i_out)), fix);
     return GD_OK;
 }
 

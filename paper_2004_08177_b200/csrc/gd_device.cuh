@@ -143,9 +143,11 @@ int launch_frontier(const double* E, const double* T, const int32_t* sm, int64_t
 int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t sm_col, int32_t mem_col, void* stream);
 
 // Walk nodes (rank form) from grid nodes; `dst` must be zeroed (padding).
+// sm_fix / mem_fix > 0: that clock column has this one value in every
+// candidate of the call, and its tests are folded into unconditional nodes.
 int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
-                            const int32_t* wroots, const double* thr, const int32_t* thr_off, WNode* dst,
-                            void* stream);
+                            const int32_t* wroots, const double* thr, const int32_t* thr_off, int32_t sm_fix,
+                            int32_t mem_fix, WNode* dst, void* stream);
 
 // Largest clock catalog the fused kernels take (32 lanes x 16 clocks).
 constexpr int kMaxClocks = 512;

@@ -409,7 +409,7 @@ __global__ void recode_clock_nodes_kernel(const PNode* __restrict__ src, PNode* 
 __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t n, const int32_t* __restrict__ roots,
                                         int32_t n_trees, const int32_t* __restrict__ wroots,
                                         const double* __restrict__ thr, const int32_t* __restrict__ thr_off,
-                                        WNode* __restrict__ dst) {
+                                        int32_t sm_fix, int32_t mem_fix, WNode* __restrict__ dst) {
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int32_t lo = 0, hi = n_trees - 1;  // last tree with roots[t] <= i
@@ -426,7 +426,16 @@ __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t 
             w.fc = static_cast<int32_t>(0xfff80000u);  // feat = kFeatLeaf
         } else {
             const int32_t child = x.aux - root;
-            if (x.feat < 0) {
+            int32_t feat = x.feat;
+            const int32_t fix = x.feat == kFeatSm ? sm_fix : (x.feat == kFeatMem ? mem_fix : 0);
+            if (fix > 0) {
+                // A clock column every candidate of the call shares: the test
+                // (double)fix <= thr has one outcome, so the node becomes an
+                // unconditional row node (feature 0; rank <= INT_MAX always
+                // goes left, rank <= -1 never) and no residue carries it.
+                feat = 0;
+                w.key = static_cast<double>(fix) <= x.v ? 0x7fffffff : -1;
+            } else if (x.feat < 0) {
                 w.key = static_cast<int32_t>(t16_of(x.v));
             } else {
                 const int32_t o = __ldg(thr_off + x.feat), c = __ldg(thr_off + x.feat + 1) - o;
@@ -437,7 +446,7 @@ __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t 
             // left child is a leaf, bit 1 the right one -- a walk stops at
             // the parent and never loads a leaf node.
             const uint32_t lf = (grid[x.aux].feat == kFeatLeaf ? 1u : 0u) | (grid[x.aux + 1].feat == kFeatLeaf ? 2u : 0u);
-            w.fc = static_cast<int32_t>((static_cast<uint32_t>(x.feat) << 19) | (static_cast<uint32_t>(child) * 8u) | lf);
+            w.fc = static_cast<int32_t>((static_cast<uint32_t>(feat) << 19) | (static_cast<uint32_t>(child) * 8u) | lf);
         }
         dst[__ldg(wroots + lo) + (i - root)] = w;
     }
@@ -522,13 +531,13 @@ int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t s
 }
 
 int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
-                            const int32_t* wroots, const double* thr, const int32_t* thr_off, WNode* dst,
-                            void* stream) {
+                            const int32_t* wroots, const double* thr, const int32_t* thr_off, int32_t sm_fix,
+                            int32_t mem_fix, WNode* dst, void* stream) {
     int blocks = static_cast<int>((n + 255) / 256);
     if (blocks > 8192) blocks = 8192;
     if (blocks < 1) blocks = 1;
     build_walk_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(grid, n, roots, n_trees, wroots,
-                                                                                  thr, thr_off, dst);
+                                                                                  thr, thr_off, sm_fix, mem_fix, dst);
     return cudaGetLastError();
 }
 

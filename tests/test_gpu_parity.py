@@ -683,3 +683,35 @@ def test_streamed_batch_inputs_vs_oracle(ctx, stream, monkeypatch):
     got2, ge, gt = gd.grid_select(me, mt, sc.grid, budgets, return_predictions=True)
     assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
     assert decisions_equal(got2, want)
+
+
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_constant_clock_columns_folded_vs_oracle(ctx, fold, monkeypatch):
+    # Catalogs whose memory (or core) clock is one value for every candidate:
+    # those tests are folded into the walk nodes (GDVFS_FOLD=1) instead of
+    # residues.  Catalogs alternate through the same models -- small calls
+    # (staged, CUDA-graph replay) and large ones -- so folded walk nodes are
+    # rebuilt, and stale graphs dropped, whenever the constancy changes.
+    monkeypatch.setenv("GDVFS_FOLD", fold)
+    sc = W.make_scenario("fold", 400, "gtx980", 60, 9, seed=41, w_clk=0.2)
+    me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
+    g = sc.grid
+    sm_all, mem_all = g.sm.astype(np.int32), g.mem.astype(np.int32)
+    one_mem = sm_all[mem_all == 3505]
+    cats = {
+        "single_mem": (one_mem, np.full(one_mem.shape, 3505, np.int32)),
+        "single_sm": (np.full(4, 1185, np.int32), np.array([405, 810, 2600, 3505], np.int32)),
+        "mixed": (sm_all, mem_all),
+        "single_mem_other": (one_mem, np.full(one_mem.shape, 810, np.int32)),
+    }
+    for rep in range(2):
+        for name, (sm, mem) in cats.items():
+            for n in (64, 400):
+                grid = W.GridInputs(g.rows[:n], g.cat_t[:n], g.cat_cols, sm, mem, g.sm_col, g.mem_col)
+                _, _, t0 = O.oracle_grid(sc.energy, sc.time, grid, np.ones(n))
+                budgets = W.deadlines_from_times(t0, seed=rep + 3)
+                want, we, wt = O.oracle_grid(sc.energy, sc.time, grid, budgets)
+                assert decisions_equal(gd.grid_select(me, mt, grid, budgets), want), (name, n, rep)
+                got, ge, gt = gd.grid_select(me, mt, grid, budgets, return_predictions=True)
+                assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt)), (name, n, rep)
+                assert decisions_equal(got, want), (name, n, rep)
