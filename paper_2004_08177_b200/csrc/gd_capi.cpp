@@ -217,6 +217,8 @@ void release_model(gd_model* m) {
     if (m->d_thr) cudaFree(m->d_thr);
     if (m->d_thr_off) cudaFree(m->d_thr_off);
     if (m->d_wroots) cudaFree(m->d_wroots);
+    if (m->d_fold) cudaFree(m->d_fold);
+    m->d_fold = nullptr;
     if (m->d_wint) cudaFree(m->d_wint);
     m->d_wint = nullptr;
     m->d_thr = nullptr;
@@ -286,11 +288,20 @@ int validate_grid(const gd_model* me, const gd_model* mt, const gd_grid* g, cons
 // The partial-evaluation kernel walks a copy of the packed nodes whose clock
 // columns are recoded (gd_device.cuh kFeatSm / kFeatMem); built once per
 // (model, sm_col, mem_col) on the context stream.
+int ensure_fold_state(gd_ctx* ctx, const gd_model* m) {
+    if (m->d_fold) return GD_OK;
+    GD_CUDA(cudaMalloc(&m->d_fold, 4 * sizeof(int32_t)), "cudaMalloc(fold state)");
+    const int32_t none[4] = {-1, -1, 1, 0};  // no state yet: the first check reports a change
+    GD_CUDA(cudaMemcpyAsync(m->d_fold, none, sizeof(none), cudaMemcpyHostToDevice, ctx->stream), "fold state");
+    return cudaStreamSynchronize(ctx->stream) == cudaSuccess ? GD_OK : set_error(GD_ERR_CUDA, "fold state sync");
+}
+
 int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t mem_col, int32_t sm_fix, int32_t mem_fix) {
     if (m->d_grid_nodes && m->grid_sm_col == sm_col && m->grid_mem_col == mem_col && m->grid_sm_fix == sm_fix &&
         m->grid_mem_fix == mem_fix)
         return GD_OK;
     if (m->packed_nodes == 0) return GD_OK;
+    if (int rc = ensure_fold_state(ctx, m)) return rc;
     if (!m->d_grid_nodes) {
         GD_CUDA(cudaMalloc(&m->d_grid_nodes, static_cast<size_t>(m->packed_nodes) * sizeof(gd::PNode)),
                 "cudaMalloc(grid nodes)");
@@ -305,9 +316,18 @@ int ensure_grid_nodes(gd_ctx* ctx, const gd_model* m, int32_t sm_col, int32_t me
     GD_CUDA(cudaMemsetAsync(m->d_wnodes, 0, static_cast<size_t>(m->n_wnodes) * sizeof(gd::WNode), ctx->stream),
             "memset(walk nodes)");
     e = gd::launch_build_walk_nodes(m->d_grid_nodes, m->packed_nodes, m->d_roots, m->n_trees(), m->d_wroots,
-                                    m->d_thr, m->d_thr_off, sm_fix, mem_fix, m->d_wnodes, ctx->stream);
+                                    m->d_thr, m->d_thr_off, sm_fix, mem_fix, nullptr, m->d_wnodes, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "walk-node kernel");
+    {  // the device mirror of the state (device-buffer calls check against it)
+        static thread_local int32_t st[4];
+        st[0] = sm_fix;
+        st[1] = mem_fix;
+        st[2] = 0;
+        st[3] = 0;
+        GD_CUDA(cudaMemcpyAsync(m->d_fold, st, sizeof(st), cudaMemcpyHostToDevice, ctx->stream), "fold state");
+        GD_CUDA(cudaStreamSynchronize(ctx->stream), "fold state sync");
+    }
     m->grid_sm_col = sm_col;
     m->grid_mem_col = mem_col;
     m->grid_sm_fix = sm_fix;
@@ -426,31 +446,55 @@ struct StreamedInputs {
     const double* budgets;
 };
 
+// Device-buffer calls: the catalog stays on the device, so the fold check runs
+// there too (launch_fold_check) and each model's walk nodes are rebuilt by a
+// kernel that exits at once unless the folded state changed -- no read-back,
+// no host sync between the caller's work and the kernels.
+int ensure_grid_nodes_device(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g) {
+    const gd_model* ms[2] = {me, mt != me ? mt : nullptr};
+    for (const gd_model* m : ms) {
+        if (!m || m->packed_nodes == 0) continue;
+        if (int rc = ensure_fold_state(ctx, m)) return rc;
+        if (!m->d_grid_nodes || m->grid_sm_col != g.sm_col || m->grid_mem_col != g.mem_col) {
+            // new clock columns: recode the grid nodes, then force a walk-node build
+            if (int rc = ensure_grid_nodes(ctx, m, g.sm_col, g.mem_col, m->grid_sm_fix, m->grid_mem_fix)) return rc;
+            const int32_t none[4] = {-1, -1, 1, 0};
+            GD_CUDA(cudaMemcpyAsync(m->d_fold, none, sizeof(none), cudaMemcpyHostToDevice, ctx->stream), "fold state");
+            GD_CUDA(cudaStreamSynchronize(ctx->stream), "fold state sync");
+        }
+    }
+    const char* env = std::getenv("GDVFS_FOLD");
+    const int enable = !(env && env[0] == '0');
+    int e = gd::launch_fold_check(g.sm_clock, g.mem_clock, g.n_clocks, enable, ms[0] ? ms[0]->d_fold : nullptr,
+                                  ms[1] ? ms[1]->d_fold : nullptr, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "fold check kernel");
+    for (const gd_model* m : ms) {
+        if (!m || m->packed_nodes == 0) continue;
+        e = gd::launch_build_walk_nodes(m->d_grid_nodes, m->packed_nodes, m->d_roots, m->n_trees(), m->d_wroots,
+                                        m->d_thr, m->d_thr_off, 0, 0, m->d_fold, m->d_wnodes, ctx->stream);
+        ++ctx->launches;
+        if (e != cudaSuccess) return cuda_error(static_cast<cudaError_t>(e), "walk-node kernel");
+        m->grid_sm_fix = m->grid_mem_fix = -2;  // known on the device only
+    }
+    return GD_OK;
+}
+
 // h_fix: the catalog's folded clocks (clock_fix) when the caller has the
-// catalog on the host; null reads it back from the device (not under capture).
+// catalog on the host; null: a device-buffer call (ensure_grid_nodes_device).
 int grid_impl(gd_ctx* ctx, const gd_model* me, const gd_model* mt, const gd_grid& g, const gd_select_opts& o,
               gd_decision* d_out, double* d_e, double* d_t, bool begin_timing = true, bool force_general = false,
               const StreamedInputs* sin = nullptr, const int32_t* h_fix = nullptr) {
     if (g.n_apps == 0) return GD_OK;
     const bool general = !takes_fast_path(me, mt, g, o, force_general);
     if (!general) {
-        int32_t fix[2] = {0, 0};
+        int rc;
         if (h_fix) {
-            fix[0] = h_fix[0];
-            fix[1] = h_fix[1];
+            rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col, h_fix[0], h_fix[1]);
+            if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col, h_fix[0], h_fix[1]);
         } else {
-            std::vector<int32_t> cat(2 * static_cast<size_t>(g.n_clocks));
-            GD_CUDA(cudaMemcpyAsync(cat.data(), g.sm_clock, g.n_clocks * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                    ctx->stream),
-                    "D2H catalog");
-            GD_CUDA(cudaMemcpyAsync(cat.data() + g.n_clocks, g.mem_clock, g.n_clocks * sizeof(int32_t),
-                                    cudaMemcpyDeviceToHost, ctx->stream),
-                    "D2H catalog");
-            GD_CUDA(cudaStreamSynchronize(ctx->stream), "catalog sync");
-            clock_fix(cat.data(), cat.data() + g.n_clocks, g.n_clocks, fix[0], fix[1]);
+            rc = ensure_grid_nodes_device(ctx, me, mt, g);
         }
-        int rc = ensure_grid_nodes(ctx, me, g.sm_col, g.mem_col, fix[0], fix[1]);
-        if (!rc) rc = ensure_grid_nodes(ctx, mt, g.sm_col, g.mem_col, fix[0], fix[1]);
         if (rc) return rc;
     }
     gd::GridParams p = grid_params(me, mt, g, o, general);

@@ -145,9 +145,15 @@ int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t s
 // Walk nodes (rank form) from grid nodes; `dst` must be zeroed (padding).
 // sm_fix / mem_fix > 0: that clock column has this one value in every
 // candidate of the call, and its tests are folded into unconditional nodes.
+// fold (device, nullable): the state written by launch_fold_check; the build
+// then runs only if that state changed.
 int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
                             const int32_t* wroots, const double* thr, const int32_t* thr_off, int32_t sm_fix,
-                            int32_t mem_fix, WNode* dst, void* stream);
+                            int32_t mem_fix, const int32_t* fold, WNode* dst, void* stream);
+// The catalog's folded clocks on the device (one block): fold[0..1] = sm /
+// mem value or 0, fold[2] = whether that changed, for up to two models.
+int launch_fold_check(const int32_t* sm, const int32_t* mem, int32_t C, int32_t enable, int32_t* fold_a,
+                      int32_t* fold_b, void* stream);
 
 // Largest clock catalog the fused kernels take (32 lanes x 16 clocks).
 constexpr int kMaxClocks = 512;

@@ -658,7 +658,7 @@ __device__ void plan_stage(const WalkParams& p, int32_t it_end, int32_t& it, int
         if (q >= ii.p1) {
             if (++it >= chunk_end) {  // next chunk
                 uint32_t nx = 0;
-                if (lane == 0) nx = atomicAdd(p.item_next, 1u);
+                if (lane == 0) nx = gridDim.x + atomicAdd(p.item_next, 1u);  // chunks past the first wave
                 it = static_cast<int32_t>(__shfl_sync(kFull, nx, 0)) * p.chunk;
                 chunk_end = min(it + p.chunk, it_end);
             }
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     };
     if (threadIdx.x == 0) {
         *pool_next = static_cast<uint32_t>(static_cast<uint64_t>(blockIdx.x) * shared_cap / gridDim.x);
-        *first_item = static_cast<int32_t>(atomicAdd(p.item_next, 1u)) * p.chunk;
+        *first_item = static_cast<int32_t>(blockIdx.x) * p.chunk;  // the first chunk is static: no atomic on the way in
         for (int b = 0; b < NB; ++b) {
             mbar_init(bar0 + 8 * b, 1);
             mbar_init(bar0 + 32 + 8 * b, nwarps);

@@ -102,7 +102,10 @@ struct gd_model {
     int32_t max_thr_per_feature = 0;
     mutable gd::WNode* d_wnodes = nullptr;
     mutable int32_t grid_sm_col = -1, grid_mem_col = -1;
-    mutable int32_t grid_sm_fix = 0, grid_mem_fix = 0;  // folded constant clocks of the walk nodes (0: none)
+    // Folded constant clocks of the walk nodes (0: none; -2: set on the device
+    // by a device-buffer call, d_fold holds them).
+    mutable int32_t grid_sm_fix = 0, grid_mem_fix = 0;
+    mutable int32_t* d_fold = nullptr;  // device {sm_fix, mem_fix, changed}
 
     int32_t n_trees() const { return offsets.empty() ? 0 : static_cast<int32_t>(offsets.size() - 1); }
 };

@@ -406,10 +406,48 @@ __global__ void recode_clock_nodes_kernel(const PNode* __restrict__ src, PNode* 
 
 // Walk nodes (gd_device.cuh WNode) from grid nodes: tree t's grid nodes
 // [roots[t], roots[t+1]) map to walk nodes [wroots[t], ...) in the same order.
+// Which clock columns are one value across the catalog (fold[0] = sm value
+// or 0, fold[1] = mem value or 0) and whether that differs from the state the
+// models' walk nodes were last built for (fold[2]); one block.
+__global__ void fold_check_kernel(const int32_t* __restrict__ sm, const int32_t* __restrict__ mem, int32_t C,
+                                  int32_t enable, int32_t* fold_a, int32_t* fold_b) {
+    __shared__ int ok_sm, ok_mem;
+    if (threadIdx.x == 0) {
+        ok_sm = 1;
+        ok_mem = 1;
+    }
+    __syncthreads();
+    const int32_t s0 = sm[0], m0 = mem[0];
+    for (int32_t c = threadIdx.x; c < C; c += blockDim.x) {
+        if (sm[c] != s0) ok_sm = 0;
+        if (mem[c] != m0) ok_mem = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int32_t smf = enable && ok_sm ? s0 : 0, memf = enable && ok_mem ? m0 : 0;
+        int32_t* folds[2] = {fold_a, fold_b};
+        for (int32_t* f : folds) {
+            if (!f) continue;
+            f[2] = f[0] != smf || f[1] != memf;
+            f[0] = smf;
+            f[1] = memf;
+        }
+    }
+}
+
+// fold (device, nullable): take sm_fix / mem_fix from fold[0..1] and build
+// only if fold[2] says the state changed (the device-buffer call path, which
+// never reads the catalog back to the host).
 __global__ void build_walk_nodes_kernel(const PNode* __restrict__ grid, int64_t n, const int32_t* __restrict__ roots,
                                         int32_t n_trees, const int32_t* __restrict__ wroots,
                                         const double* __restrict__ thr, const int32_t* __restrict__ thr_off,
-                                        int32_t sm_fix, int32_t mem_fix, WNode* __restrict__ dst) {
+                                        int32_t sm_fix, int32_t mem_fix, const int32_t* __restrict__ fold,
+                                        WNode* __restrict__ dst) {
+    if (fold) {
+        if (!fold[2]) return;
+        sm_fix = fold[0];
+        mem_fix = fold[1];
+    }
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         int32_t lo = 0, hi = n_trees - 1;  // last tree with roots[t] <= i
@@ -530,14 +568,21 @@ int launch_recode_clock_nodes(const PNode* src, PNode* dst, int64_t n, int32_t s
     return cudaGetLastError();
 }
 
+int launch_fold_check(const int32_t* sm, const int32_t* mem, int32_t C, int32_t enable, int32_t* fold_a,
+                      int32_t* fold_b, void* stream) {
+    fold_check_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(sm, mem, C, enable, fold_a, fold_b);
+    return cudaGetLastError();
+}
+
 int launch_build_walk_nodes(const PNode* grid, int64_t n, const int32_t* roots, int32_t n_trees,
                             const int32_t* wroots, const double* thr, const int32_t* thr_off, int32_t sm_fix,
-                            int32_t mem_fix, WNode* dst, void* stream) {
+                            int32_t mem_fix, const int32_t* fold, WNode* dst, void* stream) {
     int blocks = static_cast<int>((n + 255) / 256);
     if (blocks > 8192) blocks = 8192;
     if (blocks < 1) blocks = 1;
     build_walk_nodes_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(grid, n, roots, n_trees, wroots,
-                                                                                  thr, thr_off, sm_fix, mem_fix, dst);
+                                                                                  thr, thr_off, sm_fix, mem_fix, fold,
+                                                                                  dst);
     return cudaGetLastError();
 }
 

@@ -715,3 +715,30 @@ def test_constant_clock_columns_folded_vs_oracle(ctx, fold, monkeypatch):
                 got, ge, gt = gd.grid_select(me, mt, grid, budgets, return_predictions=True)
                 assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt)), (name, n, rep)
                 assert decisions_equal(got, want), (name, n, rep)
+                # the device-buffer path decides the folding on the device
+                dt = _device_grid_select(ctx, me, mt, grid, budgets)
+                assert np.array_equal(bits(dt), bits(wt)), (name, n, rep, "device path")
+
+
+def _device_grid_select(ctx, me, mt, grid, budgets):
+    """gd_grid_select_device on torch-resident copies of `grid`; returns the time table."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    n, C_ = grid.rows.shape[0], len(grid.sm)
+    keep = dict(rows=torch.from_numpy(np.ascontiguousarray(grid.rows)).to(dev),
+                cat_t=torch.from_numpy(np.ascontiguousarray(grid.cat_t)).to(dev),
+                cat_cols=torch.from_numpy(np.ascontiguousarray(grid.cat_cols, dtype=np.int32)).to(dev),
+                sm=torch.from_numpy(np.ascontiguousarray(grid.sm, dtype=np.int32)).to(dev),
+                mem=torch.from_numpy(np.ascontiguousarray(grid.mem, dtype=np.int32)).to(dev),
+                budgets=torch.from_numpy(np.ascontiguousarray(budgets)).to(dev),
+                out=torch.zeros(n * 24, dtype=torch.uint8, device=dev))
+    t_tab = torch.empty((n, C_), dtype=torch.float64, device=dev)
+    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+    try:
+        gd.grid_select_device(me, mt, {k: v.data_ptr() for k, v in keep.items()}, n, C_, grid.rows.shape[1],
+                              grid.cat_t.shape[1], grid.sm_col, grid.mem_col, t_out=t_tab.data_ptr())
+        torch.cuda.synchronize(dev)
+    finally:
+        ctx.set_stream(0)
+    return t_tab.cpu().numpy()
