@@ -49,9 +49,6 @@
 
 #include "gd_common.cuh"
 
-#ifndef GD_RES_LEVELS
-#define GD_RES_LEVELS 4  // test levels a residue table holds (deeper: FULL)
-#endif
 
 namespace gd {
 #ifdef GD_WALK_TRACE
@@ -171,6 +168,7 @@ struct WalkParams {
     RTRec* pool;
     uint32_t* pool_count;
     uint32_t pool_cap;
+    int32_t res_levels;        // test levels a residue table may hold (3 or 4; deeper: FULL)
 };
 
 // ---------------------------------------------------------------------------
@@ -492,7 +490,7 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                 }
             } else {  // a clock node at heap position P
                 const int lev = 31 - __clz(static_cast<int>(P) + 1);
-                if (lev >= GD_RES_LEVELS || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
+                if (lev >= p.res_levels || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
                     r.info = kRecFull;
                     r.ref = s.groot + (w0.n >> 3);
                     fin = true;
@@ -1944,14 +1942,15 @@ struct WalkGeom {
     size_t smem;
 };
 int64_t env_i64(const char* name, int64_t dflt);
-WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 * 1024, bool wide = false) {
+WalkGeom walk_geom(const GridParams& p, int64_t batch_apps, size_t kLimit = 227 * 1024, bool wide = false,
+                   int subs = 0) {
     WalkGeom g{};
     g.n_bufs = static_cast<int>(env_i64("GDVFS_WALK_BUFS", 2));
     g.n_bufs = g.n_bufs < 2 ? 2 : (g.n_bufs > 4 ? 4 : g.n_bufs);
     const int32_t max_tree = (p.max_wint + 1) & ~1;  // the loadable prefixes are what is staged
     // 16 warps per CTA: 16 groups x 1 warp (512 apps per tile, every warp
     // walks every tree of a stage) or 8 groups x 2 warps (even / odd trees).
-    g.n_subs = static_cast<int>(env_i64("GDVFS_WALK_SUBS", 1)) == 2 ? 2 : 1;
+    g.n_subs = static_cast<int>(env_i64("GDVFS_WALK_SUBS", subs ? subs : 1)) == 2 ? 2 : 1;
     int max_groups = static_cast<int>(env_i64("GDVFS_WALK_GROUPS", 16 / g.n_subs));
     if (max_groups > 16 / g.n_subs) max_groups = 16 / g.n_subs;
     // Small batches (the configs[4] latency stream): no more app groups than
@@ -2089,8 +2088,20 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     // parallel; fall back to the full budget if a tree pair does not fit.
     WalkGeom wg = walk_geom(p, B);
     if (wg.warps > 0 && wg.warps < 16) {
-        const WalkGeom small = walk_geom(p, B, 56 * 1024);
-        if (small.warps > 0) wg = small;
+        // Small batches: the smallest shared-memory budget that still stages a
+        // tree pair, so every work item's CTA is resident in ONE wave (the
+        // configs[4] 64-app batch has 500 one-pair items: 57 KB CTAs fit 3
+        // per SM, 444 slots -- a second wave).
+        // Two warps per 32-app group (even / odd trees): a pair whose trees
+        // put every app's walk on a clock node (a clock root) is resolved by
+        // twice the lanes -- such items are the stragglers of a latency batch.
+        for (size_t lim : {size_t(24) << 10, size_t(32) << 10, size_t(56) << 10}) {
+            const WalkGeom small = walk_geom(p, B, lim, false, 2);
+            if (small.warps > 0) {
+                wg = small;
+                break;
+            }
+        }
     }
     // 8-bit ranks (every feature of both models has <= 255 distinct
     // thresholds) and a batch that fills whole 1024-app tiles: wide tiles.
@@ -2194,6 +2205,12 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.rec[1] = rec_t;
         w.pool = pool;
         w.pool_count = counts + 2 * b;
+        // Latency batches keep residue tables to 3 test levels (deeper ones
+        // go FULL): a deep residue's depth-first resolution is the critical
+        // path of a small batch's walk.  GDVFS_RES_LEVELS overrides.
+        w.res_levels = static_cast<int32_t>(env_i64("GDVFS_RES_LEVELS", wg.warps < 16 ? 3 : 4));
+        if (w.res_levels < 1) w.res_levels = 1;
+        if (w.res_levels > 4) w.res_levels = 4;
         w.item_next = counts + 2 * b + 1;
         w.pool_cap = static_cast<uint32_t>(pool_cap);
         const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;

@@ -261,6 +261,9 @@ KNOBS = {
     "narrow_tiles": {"GDVFS_WIDE": "0"},
     "split_major": {"GDVFS_WALK_SPLIT_MAJOR": "1", "GDVFS_WALK_SPLITS": "7"},
     "tile_major": {"GDVFS_WALK_SPLIT_MAJOR": "0", "GDVFS_WALK_SPLITS": "3"},
+    "res_levels_3": {"GDVFS_RES_LEVELS": "3"},
+    "res_levels_1": {"GDVFS_RES_LEVELS": "1"},
+    "subs2": {"GDVFS_WALK_SUBS": "2"},
 }
 
 
