@@ -745,3 +745,29 @@ def _device_grid_select(ctx, me, mt, grid, budgets):
     finally:
         ctx.set_stream(0)
     return t_tab.cpu().numpy()
+
+
+@pytest.mark.parametrize("extra_cols", [70, 150])
+def test_wide_rows_walk_geometry_fallbacks(ctx, extra_cols, monkeypatch):
+    # Rows with many columns: the 8-bit 1024-app tile (F x 1024 B of ranks)
+    # or even the 512-app one no longer leaves room for a tree pair, and the
+    # walk geometry falls back to narrower tiles / fewer groups.  Streamed
+    # batches and no categorical columns on the way.
+    import dataclasses
+
+    monkeypatch.setenv("GDVFS_BATCH_BYTES", "6000000")
+    monkeypatch.setenv("GDVFS_WIDE", "2")
+    sc = W.make_scenario("wide_rows", 3000, "gtx980", 50, 9, seed=17, w_clk=0.1)
+    F = sc.grid.rows.shape[1] + extra_cols
+    rows = np.concatenate([sc.grid.rows, np.random.default_rng(1).uniform(size=(3000, extra_cols))], axis=1)
+    fe = dataclasses.replace(sc.energy, n_cols=F)
+    ft = dataclasses.replace(sc.time, n_cols=F)
+    grid = W.GridInputs(np.ascontiguousarray(rows), np.zeros((3000, 0)), np.zeros(0, np.int32), sc.grid.sm,
+                        sc.grid.mem, sc.grid.sm_col, sc.grid.mem_col)
+    me, mt = gd.Model.from_forest(fe, ctx), gd.Model.from_forest(ft, ctx)
+    _, _, t0 = O.oracle_grid(fe, ft, grid, np.ones(3000))
+    budgets = W.deadlines_from_times(t0, seed=2)
+    want, we, wt = O.oracle_grid(fe, ft, grid, budgets)
+    got, ge, gt = gd.grid_select(me, mt, grid, budgets, return_predictions=True)
+    assert np.array_equal(bits(ge), bits(we)) and np.array_equal(bits(gt), bits(wt))
+    assert decisions_equal(got, want)
