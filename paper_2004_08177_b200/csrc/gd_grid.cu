@@ -69,7 +69,7 @@ using namespace dev;
 // ---------------------------------------------------------------------------
 // The walk -> accumulate hand-off.
 // ---------------------------------------------------------------------------
-enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4, kRecTable4 = 5 };
+enum : uint32_t { kRecConst = 0, kRecSm = 1, kRecMem = 2, kRecTable = 3, kRecFull = 4, kRecTable4 = 5, kRecTable5 = 6 };
 
 // One (app, tree) record.  info = kind | t16 << 16 (SM / MEM keys); leaves
 // are referenced by packed (grid) index and their values fetched by the
@@ -106,6 +106,18 @@ struct __align__(16) RTRec4 {
     double leaf[16];
 };
 static_assert(sizeof(RTRec4) == 256, "RTRec4 is two pool slots");
+
+// A depth-5 residue (four consecutive pool slots, record kind kRecTable5):
+// tests 0..30 in heap order, leaf l (node 31 + l) at leaf[l].  Trained
+// ensembles split on the two clock columns in turn near their roots: 1.5 %
+// of a trained time model's residues have 5 test levels (per-clock traversal
+// from global memory otherwise).
+struct __align__(16) RTRec5 {
+    uint2 test[31];
+    uint32_t pad[2];
+    double leaf[32];
+};
+static_assert(sizeof(RTRec5) == 512, "RTRec5 is four pool slots");
 
 
 // Records of tree t for batch-local app la: pairs of trees are interleaved
@@ -316,11 +328,11 @@ struct PoolRegion {
     uint32_t* ovf_next;  // global, zeroed per batch
     uint32_t ovf_base, cap;
 };
-__device__ __forceinline__ uint32_t pool_take2(const PoolRegion& r) {
-    uint32_t idx = atomicAdd(r.next, 2u);
-    if (idx + 2u <= r.end) return idx;
-    idx = r.ovf_base + atomicAdd(r.ovf_next, 2u);
-    return idx + 2u <= r.cap ? idx : 0xffffffffu;
+__device__ __forceinline__ uint32_t pool_take(const PoolRegion& r, uint32_t n) {
+    uint32_t idx = atomicAdd(r.next, n);
+    if (idx + n <= r.end) return idx;
+    idx = r.ovf_base + atomicAdd(r.ovf_next, n);
+    return idx + n <= r.cap ? idx : 0xffffffffu;
 }
 
 __device__ __forceinline__ TreeSrc tree_src(const int4& te, bool all_smem) {
@@ -375,13 +387,14 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
     Job jb{0, 0, 0, 0};
     Walk w0{0, 0, 0}, cur{0, 0, 0};
     uint2 t0 = make_uint2(0u, 0u);
-    // Pending right children, a stack of at most 4: (byte offset << 8) | leaf << 7 | heap position.
-    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0, P = 1;
+    // Pending right children, a stack of at most 5: (byte offset << 8) | leaf << 7 | heap position.
+    uint32_t st0 = 0, st1 = 0, st2 = 0, st3 = 0, st4 = 0, P = 1;
     int nst = 0;
-    // The table is built in the 128-byte RTRec form and moved to the
-    // two-slot RTRec4 form only when a fourth test level appears (rare).
+    // The table is built in the 128-byte RTRec form, moved to the two-slot
+    // RTRec4 form when a fourth test level appears and to a new four-slot
+    // RTRec5 when a fifth does (both rare); L = the form's leaf depth.
     RTRec4* q = nullptr;
-    bool big = false;
+    uint32_t L = 3;
     uint32_t tmask = 1u, idx = 0;
     int maxlev = 0;
     int32_t lleaf = -1;
@@ -392,7 +405,9 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
         if (pend_dst) *pend_dst = pend_v;
         const uint32_t lev = 31u - __clz(pos + 1u);
         const uint32_t path = pos + 1u - (1u << lev);
-        pend_dst = big ? &q->leaf[path << (4u - lev)] : &reinterpret_cast<RTRec*>(q)->leaf[path << (3u - lev)];
+        pend_dst = L == 4u   ? &q->leaf[path << (4u - lev)]
+                   : L == 3u ? &reinterpret_cast<RTRec*>(q)->leaf[path << (3u - lev)]
+                             : &reinterpret_cast<RTRec5*>(q)->leaf[path << (5u - lev)];
         pend_v = __ldg(&c.gnodes[leaf_idx].v);
     };
     auto start = [&]() {  // job k: its clock node, then the left child's walk
@@ -421,7 +436,7 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
         nst = 1;
         P = 1u;
         q = nullptr;
-        big = false;
+        L = 3u;
         tmask = 1u;
         maxlev = 0;
         lleaf = -1;
@@ -457,15 +472,18 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                 }
                 if (!fin) {
                     if (nst == 0) {  // the residue is complete: its table
-                        const uint32_t D = static_cast<uint32_t>(maxlev) + 1u;  // 2, 3 or 4
+                        const uint32_t D = static_cast<uint32_t>(maxlev) + 1u;  // 2 .. 5
                         // Leaves above the last level sit under always-left tests.
 #pragma unroll
-                        for (uint32_t z = 1; z < 15; ++z) {
-                            if (z + 1u < (1u << D) && !((tmask >> z) & 1u)) q->test[z] = make_uint2(0u, 0u);
-                            if (z == 6 && D < 4) break;
+                        for (uint32_t z = 1; z < 31; ++z) {
+                            if (z + 1u < (1u << D) && !((tmask >> z) & 1u))
+                                reinterpret_cast<RTRec5*>(q)->test[z] = make_uint2(0u, 0u);
+                            if ((z == 6 && D < 4) || (z == 14 && D < 5)) break;
                         }
                         r.ref = static_cast<int32_t>(idx);
-                        if (big) {
+                        if (L == 5u) {
+                            r.info = kRecTable5;
+                        } else if (L == 4u) {
                             r.info = kRecTable4;
                         } else {
                             reinterpret_cast<RTRec*>(q)->depth = D;
@@ -477,6 +495,7 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                         st0 = st1;
                         st1 = st2;
                         st2 = st3;
+                        st3 = st4;
                         --nst;
                         P = e & 127u;
                         const int32_t n = static_cast<int32_t>(e >> 8);
@@ -490,7 +509,9 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                 }
             } else {  // a clock node at heap position P
                 const int lev = 31 - __clz(static_cast<int>(P) + 1);
-                if (lev >= p.res_levels || (!q && (idx = pool_take2(region)) == 0xffffffffu)) {
+                uint32_t idx5 = 0;
+                if (lev >= p.res_levels || (!q && (idx = pool_take(region, 2u)) == 0xffffffffu) ||
+                    (lev == 4 && L == 4u && (idx5 = pool_take(region, 4u)) == 0xffffffffu)) {
                     r.info = kRecFull;
                     r.ref = s.groot + (w0.n >> 3);
                     fin = true;
@@ -500,7 +521,7 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                         q->test[0] = t0;
                         if (lleaf >= 0) put_leaf(1u, lleaf);
                     }
-                    if (lev == 3 && !big) {  // fourth level: depth-3 leaf slot k becomes depth-4 slot 2k
+                    if (lev == 3 && L == 3u) {  // fourth level: depth-3 leaf slot k becomes depth-4 slot 2k
                         if (pend_dst) *pend_dst = pend_v;
                         pend_dst = nullptr;
                         RTRec* t = reinterpret_cast<RTRec*>(q);
@@ -509,11 +530,24 @@ __device__ __noinline__ void run_jobs(const WalkParams& p, const WalkCtx& c0, co
                         for (int z = 0; z < 8; ++z) lv[z] = t->leaf[z];
 #pragma unroll
                         for (int z = 0; z < 8; ++z) q->leaf[2 * z] = lv[z];
-                        big = true;
+                        L = 4u;
                     }
-                    q->test[P] = test_mk(cur);
+                    if (lev == 4 && L == 4u) {  // fifth level: move to four new slots, leaf k -> 2k
+                        if (pend_dst) *pend_dst = pend_v;
+                        pend_dst = nullptr;
+                        RTRec5* u = reinterpret_cast<RTRec5*>(p.pool + idx5);
+#pragma unroll
+                        for (int z = 0; z < 15; ++z) u->test[z] = q->test[z];
+#pragma unroll
+                        for (int z = 0; z < 16; ++z) u->leaf[2 * z] = q->leaf[z];
+                        q = reinterpret_cast<RTRec4*>(u);
+                        idx = idx5;
+                        L = 5u;
+                    }
+                    reinterpret_cast<RTRec5*>(q)->test[P] = test_mk(cur);
                     tmask |= 1u << P;
                     maxlev = max(maxlev, lev);
+                    st4 = st3;
                     st3 = st2;
                     st2 = st1;
                     st1 = st0;
@@ -1087,7 +1121,7 @@ struct RingT {
     static constexpr int kRv = kVal + (RS + 1) * 32 * 8;
     static constexpr int kSideOff = kRv + (RS + 1) * 32 * 8;
     static constexpr int kOvf = kSideOff + (RS + 1) * kSide * 128;
-    static constexpr int kRow = kOvf + 256;
+    static constexpr int kRow = kOvf + 512;
     __host__ __device__ static constexpr int rs(int g) { return g % (RR + 1); }  // record slot
     __host__ __device__ static constexpr int ss(int g) { return g % (RS + 1); }  // side slot
 };
@@ -1307,7 +1341,27 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
     } else {
         const uint32_t info = lds_u32(ws + RG::kMeta + slotb);
         const int32_t ref = static_cast<int32_t>(lds_u32(ws + RG::kMeta + slotb + 4));
-        if ((info & 7u) == kRecTable4) {  // rare: copied on demand (two pool slots)
+        if ((info & 7u) == kRecTable5) {  // rarer still: copied on demand (four pool slots)
+            const uint32_t sb = ws + RG::kOvf;
+            __syncwarp();
+            {
+                const int4 x = __ldg(reinterpret_cast<const int4*>(pool + ref) + lane);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * lane), "r"(x.x), "r"(x.y),
+                             "r"(x.z), "r"(x.w)
+                             : "memory");
+            }
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                uint32_t n = 0;
+#pragma unroll
+                for (int d = 0; d < 5; ++d) {
+                    const uint2 t = lds_u2(sb + n * 8u);
+                    n = 2u * n + 1u + ((ck[i] & t.x) > t.y ? 1u : 0u);
+                }
+                acc[i] = __dadd_rn(acc[i], lds_f64(sb + 256u + (n - 31u) * 8u));
+            }
+        } else if ((info & 7u) == kRecTable4) {  // rare: copied on demand (two pool slots)
             const uint32_t sb = ws + RG::kOvf;
             __syncwarp();
             if (lane < 16) {
@@ -2208,9 +2262,9 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         // Latency batches keep residue tables to 3 test levels (deeper ones
         // go FULL): a deep residue's depth-first resolution is the critical
         // path of a small batch's walk.  GDVFS_RES_LEVELS overrides.
-        w.res_levels = static_cast<int32_t>(env_i64("GDVFS_RES_LEVELS", wg.warps < 16 ? 3 : 4));
+        w.res_levels = static_cast<int32_t>(env_i64("GDVFS_RES_LEVELS", wg.warps < 16 ? 3 : 5));
         if (w.res_levels < 1) w.res_levels = 1;
-        if (w.res_levels > 4) w.res_levels = 4;
+        if (w.res_levels > 5) w.res_levels = 5;
         w.item_next = counts + 2 * b + 1;
         w.pool_cap = static_cast<uint32_t>(pool_cap);
         const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;

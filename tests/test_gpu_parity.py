@@ -262,15 +262,19 @@ KNOBS = {
     "split_major": {"GDVFS_WALK_SPLIT_MAJOR": "1", "GDVFS_WALK_SPLITS": "7"},
     "tile_major": {"GDVFS_WALK_SPLIT_MAJOR": "0", "GDVFS_WALK_SPLITS": "3"},
     "res_levels_3": {"GDVFS_RES_LEVELS": "3"},
+    "res_levels_4": {"GDVFS_RES_LEVELS": "4"},
     "res_levels_1": {"GDVFS_RES_LEVELS": "1"},
     "subs2": {"GDVFS_WALK_SUBS": "2"},
 }
 
 
+@pytest.mark.parametrize("levels", ["5", "4"])
 @pytest.mark.parametrize("w_clk,depth", [(0.25, 11), (0.4, 9), (0.15, 12)])
-def test_k2_deep_residues_tables4_and_full(ctx, w_clk, depth):
-    # clock-heavy deep trees: residues with 3-4 test levels (TABLE / TABLE4
-    # records) and deeper ones (FULL), in both accumulate modes
+def test_k2_deep_residues_tables4_and_full(ctx, w_clk, depth, levels, monkeypatch):
+    # clock-heavy deep trees: residues with 3-5 test levels (TABLE / TABLE4 /
+    # TABLE5 records) and deeper ones (FULL), in both accumulate modes, with
+    # tables up to 5 or up to 4 levels
+    monkeypatch.setenv("GDVFS_RES_LEVELS", levels)
     sc = W.make_scenario("deep_res", 300, "gtx980", 40, depth, seed=int(100 * w_clk) + depth, w_clk=w_clk)
     me, mt = gd.Model.from_forest(sc.energy, ctx), gd.Model.from_forest(sc.time, ctx)
     _, _, t0 = O.oracle_grid(sc.energy, sc.time, sc.grid, np.ones(sc.grid.n_apps))
