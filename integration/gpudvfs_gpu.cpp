@@ -618,8 +618,19 @@ thread_local const sched::ExecutionTimeSource* t_exec = nullptr;
 thread_local const std::vector<Job>* t_jobs = nullptr;
 thread_local const std::vector<ClockSet>* t_catalog = nullptr;
 
+// The last (clock, execution time) the source returned per job: the
+// decider fixpoint below re-runs the EDF loop, and a job keeping its clock
+// does not query the source again (the reference queries it once per
+// scheduled job; a pure ExecutionTimeSource gives identical values).
+thread_local std::vector<std::pair<int32_t, double>> t_exec_memo;
+
 double exec_trampoline(void*, int64_t job, int32_t clock_index) {
-    return (*t_exec)((*t_jobs)[static_cast<std::size_t>(job)], (*t_catalog)[static_cast<std::size_t>(clock_index)]);
+    auto& m = t_exec_memo[static_cast<std::size_t>(job)];
+    if (m.first == clock_index) return m.second;
+    const double v =
+        (*t_exec)((*t_jobs)[static_cast<std::size_t>(job)], (*t_catalog)[static_cast<std::size_t>(clock_index)]);
+    m = {clock_index, v};
+    return v;
 }
 
 }  // namespace
@@ -761,6 +772,7 @@ std::vector<sched::ScheduleDecision> schedule_d_dvfs(const Workload& workload, c
     t_exec = &exec;
     t_jobs = &workload.jobs;
     t_catalog = &catalog;
+    t_exec_memo.assign(static_cast<std::size_t>(n), {-1, 0.0});
     // The per-job tables live on the host here, so the O(C) scan beats
     // shipping them to the GPU for a frontier (gd_frontier pays off when the
     // tables are device-resident; scripts/edf_scale.py).
