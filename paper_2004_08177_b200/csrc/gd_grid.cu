@@ -49,6 +49,10 @@
 
 #include "gd_common.cuh"
 
+#ifndef GD_WALK_LATE_LEAF
+#define GD_WALK_LATE_LEAF 1  // 1: a root walk's leaf index is formed after its loop, not per step
+#endif
+
 
 namespace gd {
 #ifdef GD_WALK_TRACE
@@ -284,13 +288,23 @@ __device__ __forceinline__ void walkn(const WalkCtx& c, const uint32_t (&ra)[N],
             load_wnode<kAllSmem>(c, s[h], t);
             if (g[h]) {
                 w[h].n = nn;
+#if GD_WALK_LATE_LEAF
+                w[h].key = t.key;  // a leaf's packed index is filled in after the loop
+#else
                 w[h].key = lf ? s[h].groot + (nn >> 3) : t.key;
+#endif
                 w[h].fc = lf ? kLeafFc : t.fc;
             }
             g[h] = g[h] && w[h].fc >= 0;
             any |= g[h];
         }
     }
+#if GD_WALK_LATE_LEAF
+#pragma unroll
+    for (int h = 0; h < N; ++h) {
+        if (v[h] && w[h].fc == kLeafFc) w[h].key = s[h].groot + (w[h].n >> 3);
+    }
+#endif
 }
 
 // Compare key of a clock node's test (see the header comment).
