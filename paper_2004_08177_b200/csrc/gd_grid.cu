@@ -49,6 +49,9 @@
 
 #include "gd_common.cuh"
 
+#ifndef GD_TABLE_KEYS
+#define GD_TABLE_KEYS 1  // 1: per-lane compare keys for depth-2/3 tables on memory-uniform lanes
+#endif
 #ifndef GD_WALK_LATE_LEAF
 #define GD_WALK_LATE_LEAF 1  // 1: a root walk's leaf index is formed after its loop, not per step
 #endif
@@ -1268,6 +1271,42 @@ __device__ __forceinline__ void add_table(double (&acc)[CPL], const unsigned (&c
     }
 }
 
+#if GD_TABLE_KEYS
+// Lanes whose clocks share one memory clock (mem_l): every test of a table
+// becomes one unsigned compare `ck > K` -- a core-clock test keeps its key,
+// a memory-clock or always-left test has one outcome for the whole lane and
+// becomes K = 0 (right: ck >= 1 << 16) or K = ~0 (left).  Per clock the path
+// is compares and selects of per-lane keys, no per-clock test loads.
+__device__ __forceinline__ uint32_t lane_key(uint2 t, unsigned mem_l) {
+    return t.x == 0xffffffffu ? t.y : (((mem_l & t.x) > t.y) ? 0u : 0xffffffffu);
+}
+template <int CPL, int D>
+__device__ __forceinline__ void add_table_keys(double (&acc)[CPL], const unsigned (&ck)[CPL], uint32_t sb,
+                                               unsigned mem_l) {
+    const uint32_t K0 = lane_key(lds_u2(sb), mem_l), K1 = lane_key(lds_u2(sb + 8u), mem_l),
+                   K2 = lane_key(lds_u2(sb + 16u), mem_l);
+    if constexpr (D == 2) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const bool b0 = ck[i] > K0;
+            const bool b1 = ck[i] > (b0 ? K2 : K1);
+            acc[i] = __dadd_rn(acc[i], lds_f64(sb + 64u + (b0 ? 32u : 0u) + (b1 ? 16u : 0u)));
+        }
+    } else {
+        const uint32_t K3 = lane_key(lds_u2(sb + 24u), mem_l), K4 = lane_key(lds_u2(sb + 32u), mem_l),
+                       K5 = lane_key(lds_u2(sb + 40u), mem_l), K6 = lane_key(lds_u2(sb + 48u), mem_l);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const bool b0 = ck[i] > K0;
+            const bool b1 = ck[i] > (b0 ? K2 : K1);
+            const uint32_t Kl = b1 ? K4 : K3, Kr = b1 ? K6 : K5;
+            const bool b2 = ck[i] > (b0 ? Kr : Kl);
+            acc[i] = __dadd_rn(acc[i], lds_f64(sb + 64u + (b0 ? 32u : 0u) + (b1 ? 16u : 0u) + (b2 ? 8u : 0u)));
+        }
+    }
+}
+#endif
+
 // Depth-2 table when every clock of this lane has memory clock mem_l: a test
 // whose mask has no core-clock bits (a memory test, or the always-left
 // filler) has one outcome for the whole lane, so it is resolved once per lane
@@ -1293,7 +1332,11 @@ __device__ __forceinline__ void add_table2_mem_uniform(double (&acc)[CPL], const
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] > t0.y ? rv : lv);
         return;
     }
+#if GD_TABLE_KEYS
+    add_table_keys<CPL, 2>(acc, ck, sb, mem_l);
+#else
     add_table<CPL, 2>(acc, ck, sb);
+#endif
 }
 
 // The group's per-kind tree masks (ballots: warp-uniform, so the per-tree
@@ -1350,7 +1393,12 @@ __device__ __forceinline__ void add_residue(const AccModel& m, const RTRec* __re
             if (mem_uniform) add_table2_mem_uniform<CPL>(acc, ck, sb, mem_l);
             else add_table<CPL, 2>(acc, ck, sb);
         } else {
+#if GD_TABLE_KEYS
+            if (mem_uniform) add_table_keys<CPL, 3>(acc, ck, sb, mem_l);
+            else add_table<CPL, 3>(acc, ck, sb);
+#else
             add_table<CPL, 3>(acc, ck, sb);
+#endif
         }
     } else {
         const uint32_t info = lds_u32(ws + RG::kMeta + slotb);
