@@ -1320,8 +1320,14 @@ __device__ __forceinline__ void add_table2_mem_uniform(double (&acc)[CPL], const
         const uint32_t n = 1u + ((mem_l & t0.x) > t0.y ? 1u : 0u);
         const uint2 tc = lds_u2(sb + n * 8u);
         const double lv = lds_f64(sb + 64u + (2u * n - 2u) * 16u), rv = lds_f64(sb + 64u + (2u * n - 1u) * 16u);
+#if GD_TABLE_KEYS
+        const uint32_t kc = lane_key(tc, mem_l);  // one unsigned compare per clock
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], ck[i] > kc ? rv : lv);
+#else
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = __dadd_rn(acc[i], (ck[i] & tc.x) > tc.y ? rv : lv);
+#endif
         return;
     }
     const uint2 t1 = lds_u2(sb + 8u), t2 = lds_u2(sb + 16u);
