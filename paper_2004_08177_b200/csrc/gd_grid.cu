@@ -683,6 +683,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (spins > (1u << 26)) __trap();
     }
 }
+// Non-blocking probe of a barrier phase.
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(bar)
@@ -781,7 +795,10 @@ __host__ __device__ constexpr size_t walk_rank_bytes(int n_cols, int tile_apps, 
 // 8-bit ranks, tiles of 1024 apps -- each warp walks two blocks of 32 apps
 // (lane = apps li and li + 512), so a stage's trees are staged once per 1024
 // apps and a lane has twice the walks in flight.
-template <bool kAllSmem, int RB>
+//
+// kLazy: warp 0 refills a released buffer between its own walk groups rather
+// than waiting for the slowest warp before it walks (stages of many trees).
+template <bool kAllSmem, int RB, bool kLazy>
 __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant__ WalkParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -865,17 +882,31 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
     }
     for (int k = 0;; ++k) {
         const int buf = k % NB;
-        if (warp == 0) {
-            // Refill the buffer of stage k - 1 with stage k + NB - 1 once every warp released it.
+        // Warp 0 refills the buffer of stage k - 1 with stage k + NB - 1 once
+        // every warp released it.  kLazy: it probes that barrier between its
+        // own walk groups of stage k (blocking only after them), so it is not
+        // held back by the slowest warp of stage k - 1; otherwise it waits
+        // before walking.
+        if (warp == 0 && (!kLazy || k == 0)) {
             if (k >= 1) mbar_wait(bar0 + 32 + 8 * ((k - 1) % NB), static_cast<uint32_t>((k - 1) / NB) & 1u);
             produce(k + NB - 1);
             __syncwarp();
         }
+        bool produced = !(kLazy && warp == 0 && k >= 1);
+        auto poll_produce = [&](bool block) {
+            if (!kLazy || produced) return;
+            const uint32_t eb = bar0 + 32 + 8 * ((k - 1) % NB), ep = static_cast<uint32_t>((k - 1) / NB) & 1u;
+            if (block) mbar_wait(eb, ep);
+            else if (!mbar_test(eb, ep)) return;
+            produce(k + NB - 1);
+            __syncwarp();
+            produced = true;
+        };
         if (k == 0) WTRACE(2);
         mbar_wait(bar0 + 8 * buf, static_cast<uint32_t>(k / NB) & 1u);
         if (k == 0) WTRACE(3);
         const Stage s = desc[buf];
-        if (!s.valid) break;
+        if (!s.valid) break;  // every later stage is invalid too; no warp waits on one
         const ItemInfo ii = item_info(p, s.item);
         const int64_t tile0 = static_cast<int64_t>(ii.tile) * TA;
         const int n_here = static_cast<int>(min(static_cast<int64_t>(TA), p.n_apps - tile0));
@@ -935,7 +966,10 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         };
         int32_t t0 = 2 * s.q0 + sub;
 #if GD_WALK_ADAPT
-        for (; t0 + NSUB * (NW - 1) <= t_last; t0 += NW * NSUB) group(t0, std::integral_constant<int, NW>{});
+        for (; t0 + NSUB * (NW - 1) <= t_last; t0 += NW * NSUB) {
+            group(t0, std::integral_constant<int, NW>{});
+            poll_produce(false);
+        }
 #else
         for (; t0 <= t_last; t0 += NW * NSUB) group(t0, std::integral_constant<int, NW>{});
 #endif
@@ -944,7 +978,9 @@ __global__ void __launch_bounds__(512, 1) grid_walk_kernel(const __grid_constant
         else if (rest == 2) group(t0, std::integral_constant<int, (NW < 2 ? NW : 2)>{});
         else if (rest == 1) group(t0, std::integral_constant<int, 1>{});
         if (k == 0) WTRACE(4);
+        poll_produce(false);
         if (count > 0) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
+        poll_produce(true);
         if (k == 0) WTRACE(5);
         __syncwarp();
         if (lane == 0) mbar_arrive(bar0 + 32 + 8 * buf);  // this warp is done with buffer `buf`
@@ -2237,8 +2273,21 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
     // (grid_fast_path_ok routes other models to the general kernel).
     if (wg.warps == 0 || !p.rank16 || p.max_tree_nodes > 65536) return cudaErrorNotSupported;
     const bool all_smem = ((p.max_wint + 1) & ~1) <= wg.win_nodes;
-    auto walk_kern = wg.rb == 1 ? (all_smem ? grid_walk_kernel<true, 1> : grid_walk_kernel<false, 1>)
-                                : (all_smem ? grid_walk_kernel<true, 2> : grid_walk_kernel<false, 2>);
+    // Lazy refills pay off when a stage holds many trees (>= 8 of the largest
+    // window): warps then drift apart within a stage (trained ensembles'
+    // residue-heavy trees: walk -20 %, configs[1] -6 %); stages of one or two
+    // deep trees gain nothing and keep the blocking form (configs[3] +1 %).
+    // GDVFS_LAZY: 0 never, 1 auto, 2 always.
+    const int64_t lazy_knob = env_i64("GDVFS_LAZY", 1);
+    const bool lazy = lazy_knob == 2 || (lazy_knob == 1 && wg.stage_nodes >= 8 * std::max(p.max_wint, 1));
+    using WalkKern = void (*)(WalkParams);
+    WalkKern walk_kern;
+    if (wg.rb == 1)
+        walk_kern = all_smem ? (lazy ? grid_walk_kernel<true, 1, true> : grid_walk_kernel<true, 1, false>)
+                             : (lazy ? grid_walk_kernel<false, 1, true> : grid_walk_kernel<false, 1, false>);
+    else
+        walk_kern = all_smem ? (lazy ? grid_walk_kernel<true, 2, true> : grid_walk_kernel<true, 2, false>)
+                             : (lazy ? grid_walk_kernel<false, 2, true> : grid_walk_kernel<false, 2, false>);
     int walk_per_sm = occupancy(reinterpret_cast<const void*>(walk_kern), wg.warps * 32, wg.smem);
     if (walk_per_sm < 0) return cudaErrorInvalidConfiguration;
     if (walk_per_sm < 1) walk_per_sm = 1;

@@ -265,6 +265,8 @@ KNOBS = {
     "res_levels_4": {"GDVFS_RES_LEVELS": "4"},
     "res_levels_1": {"GDVFS_RES_LEVELS": "1"},
     "subs2": {"GDVFS_WALK_SUBS": "2"},
+    "lazy_refill": {"GDVFS_LAZY": "2", "GDVFS_WALK_BUFS": "3"},
+    "blocking_refill": {"GDVFS_LAZY": "0"},
 }
 
 
