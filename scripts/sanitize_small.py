@@ -2,7 +2,7 @@
 the sliced accumulate (40 apps), the main accumulate with 16-bit 512-app walk
 tiles (300 apps), 8-bit 1024-app walk tiles (1500 apps, GDVFS_WIDE=2),
 several batches with streamed inputs, a single-memory-clock catalog (folded
-walk nodes) and the device-buffer path -- each checked against the oracle.
+walk nodes), blocking and lazy stage refills and the device-buffer path -- each checked against the oracle.
 
     compute-sanitizer --tool memcheck|racecheck|synccheck python scripts/sanitize_small.py
 """
@@ -19,7 +19,8 @@ from paper_2004_08177_b200 import workload as W  # noqa: E402
 
 ctx = gd.Context(0)
 cases = [(40, {}), (300, {}), (1500, {"GDVFS_WIDE": "2"}),
-         (3000, {"GDVFS_BATCH_BYTES": "3000000", "GDVFS_WIDE": "2"}), (300, {"FOLD": "1"})]
+         (3000, {"GDVFS_BATCH_BYTES": "3000000", "GDVFS_WIDE": "2"}), (300, {"FOLD": "1"}),
+         (1500, {"GDVFS_LAZY": "0"}), (600, {"GDVFS_LAZY": "2", "GDVFS_WALK_BUFS": "3", "GDVFS_WIDE": "1"})]
 for n, env in cases:
     os.environ.update({k: v for k, v in env.items() if k.startswith("GDVFS")})
     sc = W.make_scenario("san", n, "gtx980", 40, 8, seed=5, w_clk=0.15)
