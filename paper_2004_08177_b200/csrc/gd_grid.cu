@@ -2168,14 +2168,14 @@ bool acc_sliced(int64_t n_apps) {
 }
 
 // Apps per batch: the walk -> accumulate hand-off of one batch (records,
-// residue tables, ranks) is bounded by a scratch budget (16 GiB of the 180 GB
+// residue tables, ranks) is bounded by a scratch budget (32 GiB of the 180 GB
 // HBM; it streams through HBM -- beyond a few thousand apps it does not stay
 // in L2 -- so the budget only sets how many batch boundaries, each with its
-// kernels' tail waves, a large batch pays: 4 -> 8 -> 16 GiB is -4 % / -1.5 %
-// at configs[3]).  Smaller calls allocate only what they use.
+// kernels' tail waves, a large batch pays: 4 -> 8 -> 16 -> 32 GiB is -4 % /
+// -1.5 % / -0.5 % at configs[3]).  Smaller calls allocate only what they use.
 int64_t batch_apps(const GridParams& p) {
     const int64_t per_app = grid_scratch_per_app(p);
-    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 34);
+    const int64_t budget = env_i64("GDVFS_BATCH_BYTES", int64_t(1) << 35);
     int64_t b = per_app > 0 ? budget / per_app : p.n_apps;
     b = b < 256 ? 256 : b;
     return b < p.n_apps ? b : p.n_apps;
@@ -2391,7 +2391,12 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         // configs[1] +7 %, the rank restaging per item).  GDVFS_WALK_SPLIT_MAJOR=0:
         // tile-major, ~8 items per CTA in chunks of a quarter of that.
         const bool split_major = env_i64("GDVFS_WALK_SPLIT_MAJOR", 1) != 0;
-        int64_t splits = ((split_major ? 16LL : 8LL) * sm_count + 2 * tiles - 1) / (2 * tiles);
+        // Large batches (>= 32 tiles) take ~32 items per CTA: shorter items
+        // even out the CTAs' finishing times (configs[3] -1.3 %, configs[2]
+        // -0.9 %); a small batch's items would get too short (configs[1]
+        // +9 %: the rank restaging per item) and keep ~16.
+        const int64_t items_per_cta = env_i64("GDVFS_WALK_ITEMS", split_major ? (tiles >= 32 ? 32 : 16) : 8);
+        int64_t splits = (items_per_cta * sm_count + 2 * tiles - 1) / (2 * tiles);
         splits = env_i64("GDVFS_WALK_SPLITS", splits);
         if (splits > max_pairs) splits = max_pairs;
         if (splits < 1) splits = 1;
