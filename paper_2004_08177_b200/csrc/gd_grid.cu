@@ -188,6 +188,7 @@ struct WalkParams {
     uint32_t* pool_count;
     uint32_t pool_cap;
     int32_t res_levels;        // test levels a residue table may hold (3 or 4; deeper: FULL)
+    int32_t job_run;           // queued jobs that start a run (<= kJobCap - 32)
 };
 
 // ---------------------------------------------------------------------------
@@ -372,11 +373,12 @@ struct Job {
 #ifndef GD_JOB_PAIR
 #define GD_JOB_PAIR 0
 #endif
-#ifndef GD_JOB_RUN
-#define GD_JOB_RUN 64
+#ifndef GD_JOB_CAP
+#define GD_JOB_CAP 128
 #endif
-constexpr int kJobRun = GD_JOB_RUN;  // a run starts once this many are queued (and at the end of a stage)
-constexpr int kJobCap = kJobRun + 32;  // queued jobs per warp
+// Queued jobs per warp; a run starts once WalkParams::job_run (<= cap - 32)
+// are queued, and at the end of a stage.
+constexpr int kJobCap = GD_JOB_CAP;
 
 // Resolve the queued jobs, one lane per job, depth-first: the clock node's
 // children are walked row-only to their next event (leaf or clock node); a
@@ -605,7 +607,7 @@ __device__ __forceinline__ void finish_walk(const WalkParams& p, const WalkCtx& 
     if (job) jobs[count + __popc(m & ((1u << lane) - 1u))] = Job{w.n, t, e, li};
     count += __popc(m);
     __syncwarp();
-    if (count >= kJobRun) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
+    if (count >= p.job_run) run_jobs<kAllSmem, RB>(p, c0, table, jobs, count, lane, out, tile0, region);
 }
 
 constexpr int kStageTrees = 128;  // trees per stage (table entries per buffer)
@@ -2382,6 +2384,13 @@ int launch_grid_select(const GridParams& p, bool general, int sm_count, void* st
         w.res_levels = static_cast<int32_t>(env_i64("GDVFS_RES_LEVELS", wg.warps < 16 ? 3 : 5));
         if (w.res_levels < 1) w.res_levels = 1;
         if (w.res_levels > 5) w.res_levels = 5;
+        // Runs of 96 queued jobs for stages of one or two deep trees (their
+        // refill loop keeps more lanes busy: configs[3] walk -1.6 %,
+        // configs[2] -2.4 %); 64 with lazy refills (trained configs[1]: 96
+        // costs +13 %).
+        w.job_run = static_cast<int32_t>(env_i64("GDVFS_JOB_RUN", lazy ? 64 : 96));
+        if (w.job_run > kJobCap - 32) w.job_run = kJobCap - 32;
+        if (w.job_run < 1) w.job_run = 1;
         w.item_next = counts + 2 * b + 1;
         w.pool_cap = static_cast<uint32_t>(pool_cap);
         const int64_t tiles = (n + w.tile_apps - 1) / w.tile_apps;
