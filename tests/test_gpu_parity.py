@@ -267,6 +267,8 @@ KNOBS = {
     "subs2": {"GDVFS_WALK_SUBS": "2"},
     "lazy_refill": {"GDVFS_LAZY": "2", "GDVFS_WALK_BUFS": "3"},
     "blocking_refill": {"GDVFS_LAZY": "0"},
+    "job_runs_32": {"GDVFS_JOB_RUN": "32"},
+    "job_runs_96_lazy": {"GDVFS_JOB_RUN": "96", "GDVFS_LAZY": "2"},
 }
 
 
